@@ -1,0 +1,220 @@
+/*
+ * trs_gpu.h — C ABI of the B200 term-rewriting engine (libtrs_b200.so).
+ *
+ * This is the drop-in boundary named by SURVEY.md §8(b): POD in, POD out,
+ * integer status codes, no exceptions, no torch or C++ types.  It replaces
+ * the reference's sweep engine behind its own C++ API:
+ *
+ *   SweepTrace run(TermStore&, const DispatchTable&, const SweepOptions&)
+ *                                   proj/include/trs/sweep_engine.hpp:38-47
+ *   TermStore  load(const RewriteSystem&, const Term&, uint32_t capacity)
+ *                                   proj/include/trs/term_store.hpp:47-52
+ *   Term       extract(const TermStore&)
+ *                                   proj/include/trs/term_store.hpp:54-57
+ *   DispatchTable compile(const RewriteSystem&)   proj/include/trs/dispatch.hpp:80
+ *
+ * A C++ caller keeps those signatures (see INTEGRATION.md for the adapter
+ * that flattens the reference's TermStore/DispatchTable into these structs
+ * and the one-line "gpu" branch in run_engine, proj/src/bench.cpp:49-69).
+ *
+ * Status codes map 1:1 onto the reference's error model
+ * (proj/include/trs/error.hpp:8-20):
+ *   TRS_GPU_STEP_BUDGET -> EngineError(EngineFault::StepBudget)
+ *   TRS_GPU_CAPACITY    -> EngineError(EngineFault::Capacity)
+ *   TRS_GPU_DANGLING    -> EngineError(EngineFault::DanglingReference)
+ *   TRS_GPU_INVALID     -> std::invalid_argument (bad program/store/options)
+ *   TRS_GPU_CUDA        -> CUDA runtime failure (no device, OOM, launch error)
+ *
+ * Threading: one engine handle per device, used by one host thread at a
+ * time (the reference's run is not reentrant on one store either,
+ * sweep_engine.cpp:34-46).  Distinct handles may run concurrently.
+ */
+#ifndef TRS_GPU_H
+#define TRS_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define TRS_GPU_OK 0
+#define TRS_GPU_STEP_BUDGET 1
+#define TRS_GPU_CAPACITY 2
+#define TRS_GPU_DANGLING 3
+#define TRS_GPU_INVALID 4
+#define TRS_GPU_CUDA 5
+
+#define TRS_GPU_STEP_CHECK_HEAD 0u
+#define TRS_GPU_STEP_BIND_VAR 1u
+
+/* RHS reference: TRS_GPU_REF_NODE | instruction index, or a bare var slot. */
+#define TRS_GPU_REF_NODE 0x80000000u
+
+typedef struct trs_gpu_engine trs_gpu_engine;
+
+/* One match step (reference MatchStep, dispatch.hpp:15-21).  The reference
+ * stores a child-index path from the redex root; steps run in pre-order so
+ * the node at path p.j is child j of the node an earlier CheckHead step (or
+ * the redex root) reached at path p.  `parent` is the index (within the
+ * rule) of that step, -1 for the redex root; `child` is j. */
+typedef struct trs_gpu_step {
+    uint32_t kind;   /* TRS_GPU_STEP_CHECK_HEAD / TRS_GPU_STEP_BIND_VAR */
+    int32_t parent;  /* step index within the rule, -1 = redex root */
+    uint32_t child;  /* child index at the parent */
+    uint32_t value;  /* symbol (CheckHead) or var slot (BindVar) */
+} trs_gpu_step;
+
+/* One RHS build instruction (reference RhsInstr, dispatch.hpp:40-46).
+ * Children are refs[first_ref .. first_ref + arity(symbol)). */
+typedef struct trs_gpu_instr {
+    uint32_t symbol;
+    uint32_t indegree;
+    uint32_t first_ref;
+} trs_gpu_instr;
+
+/* One compiled rule (reference CompiledRule, dispatch.hpp:66-70). */
+typedef struct trs_gpu_rule {
+    uint32_t source_order;
+    uint32_t first_step, num_steps;
+    uint32_t first_instr, num_instrs; /* topological; root last unless collapsing */
+    uint32_t num_vars;
+    uint32_t root_ref; /* TRS_GPU_REF_NODE|k (constructive) or var slot (collapse) */
+} trs_gpu_rule;
+
+/* Flattened DispatchTable (dispatch.hpp:73-78) plus the signature arities
+ * (TermStore::arity_of, term_store.hpp:19).  Rules of symbol f are
+ * rules[rule_begin[f] .. rule_begin[f+1]) in source order; first match wins
+ * (dispatch.hpp:119-130). */
+typedef struct trs_gpu_program {
+    uint32_t num_symbols;
+    const uint32_t* arity;      /* [num_symbols] */
+    const uint32_t* rule_begin; /* [num_symbols + 1] */
+    uint32_t num_rules;
+    const trs_gpu_rule* rules;
+    uint32_t num_steps;
+    const trs_gpu_step* steps;
+    uint32_t num_instrs;
+    const trs_gpu_instr* instrs;
+    uint32_t num_refs;
+    const uint32_t* refs;
+} trs_gpu_program;
+
+/* Options (reference SweepOptions, sweep_engine.hpp:29-36, plus the device
+ * knobs).  Zero-initialise and set what you need; 0 means "default". */
+typedef struct trs_gpu_options {
+    uint64_t step_budget;      /* 0 -> 1e9 (sweep_engine.hpp:32) */
+    uint32_t fixed_capacity;   /* 1: never grow; CAPACITY when the arena fills */
+    uint32_t validate;         /* 1: check the refcount ghost invariant after the run */
+    uint32_t small_enter;      /* frontier size at/below which one CTA runs the sweeps (0 -> default) */
+    uint32_t small_exit;       /* frontier size above which the whole grid takes over again */
+    uint32_t disable_small;    /* 1: never use single-CTA mode */
+    uint32_t gc_interval;      /* >0: force a compacting GC every this many sweeps (testing) */
+    uint32_t disable_gc;       /* 1: never collect (grow instead) */
+    uint32_t blocks_per_sm;    /* 0 -> occupancy maximum */
+    uint32_t record_trace;     /* 1: keep per-sweep records (default on when 0? no: 0 = on) */
+    uint32_t no_trace;         /* 1: do not keep per-sweep records */
+    uint32_t reserved[6];
+} trs_gpu_options;
+
+/* Per-sweep record (reference SweepRecord, sweep_engine.hpp:10-17).
+ * `rewrites` is the sweep width and is bit-exact to the reference;
+ * live_terms/n/free_len are allocator-dependent there and here: n is the
+ * arena bump pointer, free_len is always 0 (bump allocation + compaction
+ * leaves no free list), `active` is the size of the awake frontier list. */
+typedef struct trs_gpu_sweep_record {
+    uint32_t sweep;
+    uint32_t live_terms;
+    uint64_t rewrites;
+    uint32_t n;
+    uint32_t free_len;
+    uint32_t active;
+    uint32_t mode; /* 0 grid-wide sweep, 1 single-CTA sweep */
+    uint64_t micros_x1000; /* sweep duration in ns (device globaltimer) */
+} trs_gpu_sweep_record;
+
+typedef struct trs_gpu_stats {
+    uint64_t total_rewrites;
+    uint64_t max_width;
+    uint32_t sweeps;
+    uint32_t gc_runs;
+    uint32_t small_sweeps;     /* sweeps run by the single-CTA mode */
+    uint32_t launches;         /* kernels launched by this run (all are ours) */
+    uint32_t regrows;          /* host-side arena growths */
+    uint32_t grid_blocks;
+    uint32_t block_threads;
+    uint32_t record_words;
+    uint64_t peak_slots;       /* highest bump pointer reached */
+    uint64_t live_terms;       /* slots with refcount > 0 at the end */
+    double kernel_ms;          /* device time of the step-loop launches (CUDA events) */
+    double gc_ms;              /* device time spent inside compacting GC (globaltimer) */
+    double load_ms;            /* device time of the load kernel */
+} trs_gpu_stats;
+
+/* Number of visible CUDA devices (0 when none / no driver). */
+int trs_gpu_device_count(void);
+
+int trs_gpu_open(int device, trs_gpu_engine** out);
+void trs_gpu_close(trs_gpu_engine* engine);
+const char* trs_gpu_error_string(int status);
+/* Last detailed error message of this engine (empty when none). */
+const char* trs_gpu_last_error(trs_gpu_engine* engine);
+
+/* Stage the flattened DispatchTable in device memory (replaces the previous
+ * program).  TRS_GPU_INVALID for a malformed program or one beyond the
+ * device limits (max arity 28, 32 instructions / 48 steps / 16 vars per
+ * rule, program blob <= 40 KiB). */
+int trs_gpu_set_program(trs_gpu_engine* engine, const trs_gpu_program* program);
+
+/* Load a term store (reference TermStore layout, term_store.hpp:15-45):
+ * slots [1, n) hold terms, slot 0 is never a term; hss[i] is the head
+ * symbol; args is column-major, args[j * n + i] for j < max_arity (0 =
+ * absent); refcounts already include one pin per root.  `roots` lists the
+ * root slots (one per independent term).  capacity 0 sizes the arena
+ * automatically; an explicit capacity < n fails with TRS_GPU_CAPACITY
+ * (term_store.cpp:50-53).  Buffers are HOST pointers; they are copied. */
+int trs_gpu_load(trs_gpu_engine* engine, uint32_t n, const uint32_t* roots, uint32_t num_roots,
+                 const uint32_t* hss, const uint32_t* args, uint32_t max_arity,
+                 const uint32_t* refcounts, uint64_t capacity);
+
+/* Same, from DEVICE pointers already resident in HBM (bench `value` path). */
+int trs_gpu_load_device(trs_gpu_engine* engine, uint32_t n, const uint32_t* roots,
+                        uint32_t num_roots, const uint32_t* d_hss, const uint32_t* d_args,
+                        uint32_t max_arity, const uint32_t* d_refcounts, uint64_t capacity);
+
+/* Normalise every loaded root (reference run, sweep_engine.cpp:428-430).
+ * Synchronous.  On TRS_GPU_STEP_BUDGET / TRS_GPU_CAPACITY the store is left
+ * as the failing sweep left it, like the reference. */
+int trs_gpu_run(trs_gpu_engine* engine, const trs_gpu_options* options, trs_gpu_stats* stats);
+
+/* Per-sweep records of the last run; *count receives the number of records
+ * (copies min(count, cap)). */
+int trs_gpu_trace(trs_gpu_engine* engine, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count);
+
+/* Canonical DAG words of root `root_index` (pre-order from
+ * the root, children left to right, ids on first visit, words = symbol then
+ * child ids per id).  Two-call protocol: if cap < needed, nothing is copied
+ * and *n_words receives the size.  TRS_GPU_DANGLING when the root's graph
+ * references slot 0 or a dead slot (term_store.cpp:84-88). */
+int trs_gpu_canonical(trs_gpu_engine* engine, uint32_t root_index, uint32_t* words, uint64_t cap,
+                      uint64_t* n_words, uint32_t* n_nodes);
+
+/* Raw store copy-back (reference TermStore layout): after a compacting pass
+ * the live slots are renumbered 1..n-1 in their arena order, roots updated.
+ * Pass NULL arrays to query n first.  args is column-major [max_arity * n]. */
+int trs_gpu_fetch_store(trs_gpu_engine* engine, uint32_t* n, uint32_t* roots, uint32_t* hss,
+                        uint32_t* args, uint32_t* refcounts, uint8_t* nf, uint32_t cap);
+
+/* Device-side roofline probe: `iters` launches of a uniformly random 4-byte
+ * (bytes_per_access = 4), 8-byte or 16-byte gather over a `bytes`-sized
+ * array in HBM (indices streamed coalesced).  Returns achieved GB/s counting
+ * bytes_per_access per access. */
+int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters,
+                         double* gbps);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TRS_GPU_H */
