@@ -1,0 +1,430 @@
+#!/usr/bin/env python
+"""Benchmark: config 5 of BASELINE.json -- 8 shards x 4096 independent fib
+roots (5F; `--workload sort` for the tree-merge-sort variant 5S), normalised
+on the B200 engine, shards split across the ranks (strong scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one full normalisation of this rank's shards (all roots loaded as
+one multi-root store).  `value` = rewrites of all ranks / max-over-ranks
+device time, inputs already resident in HBM (device SoA -> engine load
+kernel -> step loop), L2 flushed before every step.  `e2e` = the same
+through the host C ABI with pinned host buffers: H2D of the SoA store, load,
+step loop, device compaction, D2H of the normal-form arena.
+"Measurement" for the roofline byte model.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "rewrites/sec and achieved random-gather HBM GB/s (% of roofline) vs host CPU"
+COUNTS = os.path.join(ROOT, "tests", "golden", "workload_counts.json")
+PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "traffic.json")
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--workload", choices=["fib", "sort"], default="fib")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-GPU table")
+    ap.add_argument("--configs-only", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def my_shards(rank: int, world: int, total: int = 8):
+    lo = rank * total // world
+    hi = (rank + 1) * total // world
+    return list(range(lo + 1, hi + 1))  # seeds
+
+
+def load_counts():
+    if os.path.exists(COUNTS):
+        with open(COUNTS) as f:
+            return json.load(f)
+    return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", str(self.device)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6544.3), "measured"
+    return 6650.0, "fallback"
+
+
+def cpu_baseline_reference(texts):
+    """The unmodified reference seq engine (oracle/_ref), one thread per shard,
+    all shards concurrently (nproc concurrent seq processes)."""
+    from oracle import ref
+
+    if ref.available():
+        wall, rewrites, status = ref.run_many(texts, "seq")
+        assert all(s == 0 for s in status), status
+        return {"value": sum(rewrites) / wall, "unit": "rewrites/s", "cores": len(texts), "kind": "reference",
+                "sample": f"{len(texts)} shards x 4096 roots, reference seq engine (seq_engine.cpp), "
+                          f"one thread per shard, {wall:.2f} s wall", "seconds": wall,
+                "host_cpus": os.cpu_count()}
+    from oracle import oracle as port
+
+    t = time.time()
+    total = 0
+    for tx in texts[:2]:
+        total += port.run_seq(tx, words=False).rewrites
+    wall = time.time() - t
+    return {"value": total / wall, "unit": "rewrites/s", "cores": 1, "kind": "port",
+            "sample": "2 shards through the C oracle seq restatement, 1 thread", "seconds": wall,
+            "host_cpus": os.cpu_count()}
+
+
+def run_reference(args, texts_all):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from oracle import ref
+
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtrs_ref.so not built"}))
+        return
+    vals = []
+    total_rw = 0
+    for k in range(args.warmup + args.steps):
+        wall, rw, st = ref.run_many(texts_all, "seq")
+        assert all(s == 0 for s in st)
+        if k >= args.warmup:
+            vals.append((sum(rw), wall))
+            total_rw = sum(rw)
+    t = sum(w for _, w in vals)
+    value = sum(r for r, _ in vals) / t
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "rewrites/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(vals),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args, len(texts_all)),
+        "cpu_baseline": {"value": value, "unit": "rewrites/s", "cores": len(texts_all), "kind": "reference",
+                         "sample": f"{len(texts_all)} shards, unmodified reference seq engine, one thread per "
+                                   f"shard, full workload per step ({total_rw} rewrites)",
+                         "host_cpus": os.cpu_count()},
+        "e2e": {"value": value, "unit": "rewrites/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def workload_config(args, nshards):
+    name = "fibbatch" if args.workload == "fib" else "treemergesort-batch"
+    return {"workload": f"config 5{'F' if args.workload == 'fib' else 'S'}: {name} {nshards} shards x 4096 "
+                        f"independent roots (seeds 1..{nshards})",
+            "shards": nshards, "roots_per_shard": 4096, "parallelism": "shards (no inter-GPU traffic)",
+            "l2": "flushed between timed steps (512 MiB write on the engine stream)"}
+
+
+def per_config_table(eng, api, W, counts, hbm_peak, gather_gbps):
+    """Single-GPU timing + parity of every BASELINE config (one warm-up, one timed run)."""
+    import torch
+
+    out = {}
+    names = ["fib18", "mergesort16k", "transform22", "buildsum22", "reverse16k", "ackermann36"]
+    for name in names:
+        text = W.CONFIGS[name][0]()
+        sysm = api.System(text)
+        store = api.Store.load(sysm)
+        eng.set_program(sysm)
+        best = None
+        for rep in range(2):
+            eng.load(store)
+            st = eng.run()
+            best = st
+        tr = eng.trace()
+        widths = tr["rewrites"].astype("<u8")
+        import hashlib
+
+        c = counts.get(name)
+        t = best["kernel_ms"] * 1e-3
+        row = {"rewrites": best["total_rewrites"], "sweeps": best["sweeps"], "kernel_ms": best["kernel_ms"],
+               "rewrites_per_s": best["total_rewrites"] / t, "us_per_sweep": 1e6 * t / best["sweeps"],
+               "small_sweeps": best["small_sweeps"], "gc_runs": best["gc_runs"]}
+        if c:
+            row["parity_rewrites"] = c["rewrites"] == best["total_rewrites"]
+            row["parity_widths"] = c["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
+            a = c["A"]
+            row["gather_gbps"] = 4 * a / t / 1e9
+            row["gather_frac"] = row["gather_gbps"] / gather_gbps if gather_gbps else None
+            row["dram_model_gbps"] = (32 * a + c["S_min"]) / t / 1e9
+            row["dram_model_frac"] = row["dram_model_gbps"] / hbm_peak
+            t_roof = max(4 * a / (gather_gbps * 1e9) if gather_gbps else 0, c["S_min"] / (hbm_peak * 1e9))
+            row["t_roof_frac"] = t_roof / t
+        out[name] = row
+        del store, sysm
+        torch.cuda.synchronize()
+    return out
+
+
+def main():
+    args = parse_args()
+    world, rank, local = dist_env()
+    from paper_2009_07174_b200 import workloads as W
+
+    kind = args.workload
+    seeds_all = list(range(1, 9))
+    mk = W.fib_batch if kind == "fib" else W.treemergesort_batch
+    if args.impl == "reference":
+        run_reference(args, [mk(s) for s in seeds_all])
+        return
+
+    import torch
+
+    from paper_2009_07174_b200 import api
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    seeds = my_shards(rank, world)
+    texts = [mk(s) for s in seeds]
+    systems = [api.System(t) for t in texts]
+    store = api.Store.load(systems)
+    v = store.view()
+    eng = api.Engine(local)
+    eng.set_program(systems[0])
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+
+    # device-resident inputs (value path) and pinned host inputs (e2e path)
+    d_hss = torch.from_numpy(v["hss"].view(np.int32)).to(dev)
+    d_args = torch.from_numpy(v["args"].view(np.int32)).to(dev)
+    d_rc = torch.from_numpy(v["refcounts"].view(np.int32)).to(dev)
+    roots = v["roots"].copy()
+    p_hss = torch.from_numpy(v["hss"].view(np.int32)).pin_memory()
+    p_args = torch.from_numpy(v["args"].view(np.int32)).pin_memory()
+    p_rc = torch.from_numpy(v["refcounts"].view(np.int32)).pin_memory()
+    p_roots = torch.from_numpy(roots.view(np.int32)).pin_memory()
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    torch.cuda.synchronize()
+
+    def step_value():
+        eng.load_device(v["n"], roots, d_hss.data_ptr(), d_args.data_ptr(), v["maxarity"], d_rc.data_ptr())
+        return eng.run()
+
+    # ---- warm-up (also sizes the arena once so no growth happens inside timing)
+    for _ in range(args.warmup):
+        st = step_value()
+    torch.cuda.synchronize()
+
+    # ---- timed: device-resident inputs
+    evs = []
+    stats = []
+    with ClockSampler(local) as clocks:
+        if world > 1:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+            stats.append(step_value())
+            e1.record(stream)
+            evs.append((e0, e1))
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    my_ms = sum(step_ms)
+    my_rewrites = sum(s["total_rewrites"] for s in stats)
+    tot = torch.tensor([my_ms], dtype=torch.float64, device=dev)
+    rw = torch.tensor([my_rewrites], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(rw, op=torch.distributed.ReduceOp.SUM)
+    max_ms = tot.item()
+    all_rw = rw.item()
+    value = all_rw / (max_ms * 1e-3)
+    launches = sum(2 + s["launches"] for s in stats)  # load_records + load_frontier + step loop(s)
+
+    # ---- e2e: pinned host buffers through the C ABI, D2H of the normal-form store
+    h2d = (p_hss.numel() + p_args.numel() + p_rc.numel() + p_roots.numel()) * 4
+    d2h_bytes = []
+    e2e_ms = []
+    host_out = None
+    for k in range(args.warmup + args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        rc = api.lib().trs_gpu_load(eng._h, v["n"], p_roots.data_ptr(), len(roots), p_hss.data_ptr(),
+                                    p_args.data_ptr(), v["maxarity"], p_rc.data_ptr(), 0)
+        assert rc == 0, eng._err()
+        s_run = eng.run()
+        s_cmp = eng.compact(8)
+        nbytes, _ = eng.fetch_records()
+        if host_out is None or host_out.numel() < nbytes:
+            host_out = torch.empty(max(nbytes, 1 << 20) * 2, dtype=torch.uint8).pin_memory()
+        eng.fetch_records(host_out.data_ptr(), host_out.numel())
+        e1.record(stream)
+        e1.synchronize()
+        if k >= args.warmup:
+            e2e_ms.append(e0.elapsed_time(e1))
+            d2h_bytes.append(nbytes)
+            launches_e2e = 2 + s_run["launches"] + s_cmp["launches"]
+    e2e_tot = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        torch.distributed.all_reduce(e2e_tot, op=torch.distributed.ReduceOp.MAX)
+    e2e_value = all_rw / (e2e_tot.item() * 1e-3)
+
+    # parity of this rank's shards against the reference-derived fixture
+    counts = load_counts()
+    key = "fibbatch" if kind == "fib" else "sortbatch"
+    fx = [counts.get(f"{key}_s{s}") for s in seeds]
+    parity = None
+    if all(fx):
+        parity = {"rewrites_match": int(sum(c["rewrites"] for c in fx)) == int(stats[-1]["total_rewrites"]),
+                  "reference_rewrites": int(sum(c["rewrites"] for c in fx)),
+                  "sweeps_match": max(c["sweeps"] for c in fx) == int(stats[-1]["sweeps"])}
+
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+
+    hbm_peak, peak_kind = measured_peaks()
+    gather_gbps = api.gather_probe(local, 4 << 30, 4, 5)
+    kernel_ms = statistics.mean(s["kernel_ms"] for s in stats)
+    roofline = None
+    if all(fx):
+        A = sum(c["A"] for c in fx)
+        smin = sum(c["S_min"] for c in fx)
+        t = kernel_ms * 1e-3
+        alg_bytes = 32 * A + smin
+        traffic = None
+        if os.path.exists(PROFILE_SUMMARY):
+            with open(PROFILE_SUMMARY) as f:
+                traffic = json.load(f).get(f"{key}_{len(seeds)}shards")
+        roofline = {
+            "bound": "hbm", "achieved": alg_bytes / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": alg_bytes / t / 1e9 / hbm_peak, "traffic": traffic,
+            "kernel": "step_loop<8> (persistent cooperative sweep loop)",
+            "algorithmic_bytes_per_launch": alg_bytes,
+            "byte_model": "32 B x A (one DRAM sector per random access) + S_min (frontier streaming), "
+                          "SURVEY.md 8(d); A, S_min from the C oracle (tests/golden/workload_counts.json)",
+            "peak_kind": peak_kind,
+            "gather": {"achieved_gbps": 4 * A / t / 1e9, "roofline_gbps": gather_gbps,
+                       "frac": 4 * A / t / 1e9 / gather_gbps,
+                       "definition": "4 B x A / step-loop time vs measured uniformly random 4-B gather over "
+                                     "4 GiB (trs_gpu_gather_probe)"},
+            "t_roof_frac": max(4 * A / (gather_gbps * 1e9), smin / (hbm_peak * 1e9)) / t,
+        }
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_reference([mk(s) for s in seeds_all])
+    configs = None
+    if world == 1 and not args.no_configs:
+        configs = per_config_table(eng, api, W, counts, hbm_peak, gather_gbps)
+    line = {
+        "metric": METRIC, "value": value, "unit": "rewrites/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args, 8),
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "e2e": {"value": e2e_value, "unit": "rewrites/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": int(statistics.mean(d2h_bytes)),
+                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_compact + trs_gpu_fetch_records "
+                        "(pinned host), CUDA events on the engine stream", "ms_per_step": statistics.mean(e2e_ms),
+                "gpu_launches_per_step": launches_e2e},
+        "gpu_launches": launches,
+        "clocks": clocks.summary(),
+        "parity": parity,
+        "engine": {"sweeps": stats[-1]["sweeps"], "small_sweeps": stats[-1]["small_sweeps"],
+                   "gc_runs": stats[-1]["gc_runs"], "grid_blocks": stats[-1]["grid_blocks"],
+                   "block_threads": stats[-1]["block_threads"], "record_words": stats[-1]["record_words"],
+                   "peak_slots": stats[-1]["peak_slots"], "kernel_ms": kernel_ms,
+                   "step_ms": step_ms},
+        "per_config": configs,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -113,9 +113,10 @@ typedef struct trs_gpu_options {
     uint32_t gc_interval;      /* >0: force a compacting GC every this many sweeps (testing) */
     uint32_t disable_gc;       /* 1: never collect (grow instead) */
     uint32_t blocks_per_sm;    /* 0 -> occupancy maximum */
-    uint32_t record_trace;     /* 1: keep per-sweep records (default on when 0? no: 0 = on) */
-    uint32_t no_trace;         /* 1: do not keep per-sweep records */
-    uint32_t reserved[6];
+    uint32_t variant;          /* step-loop register budget: 0/1 = 1 CTA/SM no spills, 2 = 2 CTAs/SM */
+    uint32_t max_blocks;       /* >0: cap the persistent grid (profiling the single-CTA mode) */
+    uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters) */
+    uint32_t reserved[5];
 } trs_gpu_options;
 
 /* Per-sweep record (reference SweepRecord, sweep_engine.hpp:10-17).
@@ -205,6 +206,25 @@ int trs_gpu_canonical(trs_gpu_engine* engine, uint32_t root_index, uint32_t* wor
  * Pass NULL arrays to query n first.  args is column-major [max_arity * n]. */
 int trs_gpu_fetch_store(trs_gpu_engine* engine, uint32_t* n, uint32_t* roots, uint32_t* hss,
                         uint32_t* args, uint32_t* refcounts, uint8_t* nf, uint32_t cap);
+
+/* The CUDA stream (cudaStream_t) every call of this engine runs on, for
+ * callers that bracket calls with their own CUDA events. */
+void* trs_gpu_stream(trs_gpu_engine* engine);
+
+/* Debug phase counters of the last runs (cycles summed over sweeps of CTA
+ * 0's thread 0): match, claim, apply, push, whole single-CTA sweep, sweeps. */
+int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out6);
+
+/* Compacting collection on demand (up to max_rounds passes, 0 -> 8, stops
+ * when a pass reclaims nothing): afterwards the arena holds only slots
+ * still referenced, renumbered densely, roots updated. */
+int trs_gpu_compact(trs_gpu_engine* engine, uint32_t max_rounds, trs_gpu_stats* stats);
+
+/* Raw copy of the device arena [0, n) into dst (record_words u32 per slot:
+ * head|cursor<<24, nf epoch, refcount, waiter, args...) and of the root
+ * slots into roots_out (may be NULL).  Two-call protocol on cap_bytes. */
+int trs_gpu_fetch_records(trs_gpu_engine* engine, void* dst, uint64_t cap_bytes, uint64_t* bytes,
+                          uint32_t* record_words, uint32_t* roots_out);
 
 /* Device-side roofline probe: `iters` launches of a uniformly random 4-byte
  * (bytes_per_access = 4), 8-byte or 16-byte gather over a `bytes`-sized

@@ -59,9 +59,10 @@ class Options(ctypes.Structure):
         ("gc_interval", ctypes.c_uint32),
         ("disable_gc", ctypes.c_uint32),
         ("blocks_per_sm", ctypes.c_uint32),
-        ("record_trace", ctypes.c_uint32),
-        ("no_trace", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32 * 6),
+        ("variant", ctypes.c_uint32),
+        ("max_blocks", ctypes.c_uint32),
+        ("profile", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32 * 5),
     ]
 
 
@@ -121,6 +122,10 @@ def lib():
         "trs_gpu_canonical": ([P, U32, P, U64, ctypes.POINTER(U64), u32p], I),
         "trs_gpu_fetch_store": ([P, u32p, P, P, P, P, P, U32], I),
         "trs_gpu_gather_probe": ([I, U64, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
+        "trs_gpu_stream": ([P], P),
+        "trs_gpu_profile_counters": ([P, P], I),
+        "trs_gpu_compact": ([P, U32, ctypes.POINTER(Stats)], I),
+        "trs_gpu_fetch_records": ([P, P, U64, ctypes.POINTER(U64), u32p, P], I),
         "trsb_system_load": ([ctypes.c_char_p, ctypes.POINTER(P), ctypes.c_char_p, ctypes.c_size_t], I),
         "trsb_system_free": ([P], None),
         "trsb_num_symbols": ([P], U32),
@@ -157,7 +162,8 @@ def exported_symbols() -> list[str]:
     return [n for n in ("trs_gpu_device_count", "trs_gpu_open", "trs_gpu_close", "trs_gpu_error_string",
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
                         "trs_gpu_run", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
-                        "trs_gpu_gather_probe")]
+                        "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
+                        "trs_gpu_profile_counters")]
 
 
 def device_count() -> int:
@@ -424,6 +430,31 @@ class Engine:
         rc = lib().trs_gpu_run(self._h, ctypes.byref(options or Options()), ctypes.byref(st))
         _raise(rc, self._err())
         return st.as_dict()
+
+    @property
+    def stream(self) -> int:
+        """cudaStream_t of this engine (for torch.cuda.ExternalStream + events)."""
+        return lib().trs_gpu_stream(self._h)
+
+    def profile_counters(self) -> dict:
+        out = np.zeros(6, np.uint64)
+        lib().trs_gpu_profile_counters(self._h, out.ctypes.data)
+        keys = ("match", "claim", "apply", "push", "sweep", "sweeps")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+    def compact(self, max_rounds: int = 8) -> dict:
+        st = Stats()
+        rc = lib().trs_gpu_compact(self._h, max_rounds, ctypes.byref(st))
+        _raise(rc, self._err())
+        return st.as_dict()
+
+    def fetch_records(self, dst_ptr: int | None = None, cap_bytes: int = 0, roots_ptr: int | None = None):
+        """Raw arena copy into a (pinned) host buffer; returns (bytes, record_words)."""
+        nb = ctypes.c_uint64(0)
+        rw = ctypes.c_uint32(0)
+        rc = lib().trs_gpu_fetch_records(self._h, dst_ptr, cap_bytes, ctypes.byref(nb), ctypes.byref(rw), roots_ptr)
+        _raise(rc, self._err())
+        return nb.value, rw.value
 
     def trace(self) -> np.ndarray:
         n = ctypes.c_uint64(0)

@@ -58,6 +58,21 @@ enum Status : uint32_t {
     kNeedTrace = 5,
 };
 
+struct __align__(16) SweepCtr {
+    uint32_t count;  // frontier list length of sweep s
+    uint32_t alloc;  // slots claimed during sweep s
+    unsigned long long rew;  // rewrites of sweep s
+};
+
+__device__ __forceinline__ SweepCtr ld_ctr(const SweepCtr* p) {
+    uint4 v = __ldcg(reinterpret_cast<const uint4*>(p));
+    SweepCtr c;
+    c.count = v.x;
+    c.alloc = v.y;
+    c.rew = (unsigned long long)v.z | ((unsigned long long)v.w << 32);
+    return c;
+}
+
 // Control block in device memory.  Persistent fields are written only at
 // quiescent points (kernel exit, single-CTA hand-back); per-sweep counters
 // rotate over 4 sweeps so that resetting the one two sweeps ahead never
@@ -74,20 +89,19 @@ struct Ctl {
     uint32_t abort_capacity;
     unsigned long long total_rewrites;
     unsigned long long max_width;
-    long long live;
     unsigned long long gc_ns;
     uint32_t peak_base;
     uint32_t last_gc_sweep;
-    // barrier
-    uint32_t bar_count;
-    uint32_t bar_gen;
-    // rotating per-sweep counters (index sweep & 3)
-    uint32_t count[4];  // frontier list length of sweep s
-    uint32_t alloc[4];  // slots claimed during sweep s
-    unsigned long long rew[4];
-    unsigned long long dead[4];
+    // barrier: monotonic arrival counter, reset by the host before a launch
+    uint32_t bar_arrive;
+    uint32_t bar_pad;
+    // rotating per-sweep counters (index sweep & 3), one 16-byte load each
+    SweepCtr ctr[4];
     // GC scratch
     uint32_t gc_live;
+    uint32_t prof_pad;
+    // phase cycle accounting (P.profile): match, claim, apply, push, sweep total, sweeps
+    unsigned long long prof[6];
 };
 
 struct Params {
@@ -110,6 +124,9 @@ struct Params {
     uint32_t fixed_capacity;
     uint32_t max_new;
     uint32_t sweep0;  // sweeps completed before this run (epochs keep counting)
+    uint32_t compact_only;  // >0: run at most this many compaction rounds and exit
+    uint32_t prefer_grow;   // out of headroom: grow (host) rather than collect
+    uint32_t profile;       // phase cycle accounting of CTA 0 (debug)
 };
 
 __device__ __forceinline__ uint32_t ld_cg(const uint32_t* p) { return __ldcg(p); }
@@ -128,18 +145,26 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
     return v;
 }
 
-__device__ void grid_sync(Ctl* ctl, uint32_t nblocks) {
+// Software grid barrier (all CTAs are co-resident: cooperative launch).
+// Arrivals are fire-and-forget increments of one monotonic counter; the
+// k-th barrier completes when it reaches k * nblocks, so nobody resets it.
+// `park` is for CTAs idling while CTA 0 runs single-CTA sweeps: they back
+// off to microsecond sleeps so their polling does not load the L2 slice
+// CTA 0 is working against.
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ void grid_sync(Ctl* ctl, uint32_t nblocks, uint32_t& epoch, bool park = false) {
     __syncthreads();
+    ++epoch;
     if (threadIdx.x == 0) {
-        uint32_t gen = ld_acquire(&ctl->bar_gen);
-        __threadfence();
-        uint32_t arrived = atomicAdd(&ctl->bar_count, 1u) + 1;
-        if (arrived == nblocks) {
-            atomicExch(&ctl->bar_count, 0u);
-            __threadfence();
-            atomicAdd(&ctl->bar_gen, 1u);
-        } else {
-            while (ld_acquire(&ctl->bar_gen) == gen) __nanosleep(20);
+        red_release_add(&ctl->bar_arrive, 1u);
+        const uint32_t target = epoch * nblocks;
+        uint32_t ns = 32;
+        while ((int)(ld_acquire(&ctl->bar_arrive) - target) < 0) {
+            __nanosleep(ns);
+            if (park && ns < 4096) ns <<= 1;
         }
         __threadfence();
     }
@@ -263,7 +288,9 @@ enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild };
 
 struct Acc {
     unsigned long long rewrites = 0;
-    unsigned long long dead = 0;
+    // optional phase accounting (thread 0 of CTA 0, P.profile): cycles in
+    // [0] match, [1] claim, [2] apply, [3] push
+    long long t[4] = {0, 0, 0, 0};
 };
 
 // One sweep over frontier entries [0, m) of `in`, by CTAs block_rank,
@@ -273,9 +300,11 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
                               uint32_t s, uint32_t m, const uint32_t* __restrict__ in,
                               uint32_t* __restrict__ out, uint32_t* out_count, uint32_t base,
                               uint32_t* alloc_ctr, uint32_t block_rank, uint32_t nblocks,
-                              Acc& acc) {
+                              Acc& acc, uint32_t* abort_flag = nullptr) {
     constexpr int MAXA = W - 4;
+    const bool prof = P.profile && threadIdx.x == 0 && block_rank == 0;
     for (uint32_t start = block_rank * kBlock; start < m; start += nblocks * kBlock) {
+        long long c0 = prof ? clock64() : 0;
         const uint32_t idx = start + threadIdx.x;
         uint32_t act = kActNone;
         uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
@@ -354,6 +383,8 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
             }
         }
 
+        long long c1 = prof ? clock64() : 0;
+        if (prof) acc.t[0] += c1 - c0;
         // ---- allocation: one claim per CTA iteration (get_new_index, term_store.cpp:118-138)
         uint32_t need = act == kActBuild ? G.rules[rule].new_slots : 0;
         uint32_t total;
@@ -365,9 +396,12 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
         if (act == kActBuild && (uint64_t)fresh + need > P.capacity) {
             // fixed capacity exhausted: the reference raises Capacity (sweep_engine.cpp:221-226)
             atomicExch(&P.ctl->abort_capacity, 1u);
+            if (abort_flag) *abort_flag = 1u;
             act = kActNone;
         }
 
+        long long c2 = prof ? clock64() : 0;
+        if (prof) acc.t[1] += c2 - c1;
         // ---- apply (sweep_engine.cpp:190-258)
         uint32_t npush = 0, push1 = 0, push_mask = 0;
         if (act == kActWait) {
@@ -404,7 +438,7 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
                 if ((uint32_t)j < sar) atomicAdd(rec<W>(arena, b[j]) + kWRc, 1u);
 #pragma unroll
             for (int j = 0; j < MAXA; ++j)
-                if ((uint32_t)j < ar && atomicSub(rec<W>(arena, a[j]) + kWRc, 1u) == 1u) acc.dead++;
+                if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
             uint32_t w = atomicExch(R + kWWaiter, kWoken);
             if (w != 0 && w != kWoken) {
                 npush = 1;
@@ -453,13 +487,15 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
             }
 #pragma unroll
             for (int j = 0; j < MAXA; ++j)
-                if ((uint32_t)j < ar && atomicSub(rec<W>(arena, a[j]) + kWRc, 1u) == 1u) acc.dead++;
+                if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
             push_mask = Rl.push_mask;
             npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
             push1 = i;
             acc.rewrites++;
         }
 
+        long long c3 = prof ? clock64() : 0;
+        if (prof) acc.t[2] += c3 - c2;
         // ---- next frontier: one reservation per CTA iteration
         uint32_t ptotal;
         uint32_t pexcl = block_scan(npush, &ptotal, sm);
@@ -480,6 +516,7 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
                 out[pos] = push1;
             }
         }
+        if (prof) acc.t[3] += clock64() - c3;
     }
 }
 
@@ -489,17 +526,12 @@ __device__ void process_sweep(const Params& P, const Prog& G, Smem& sm, uint32_t
 template <int W>
 __device__ uint32_t gc_compact(const Params& P, Smem& sm, uint32_t& arena_idx, uint32_t base,
                                uint32_t cur_list, uint32_t m, uint32_t block_rank,
-                               uint32_t nblocks, const Prog& G, bool grid) {
+                               uint32_t nblocks, const Prog& G, uint32_t& epoch) {
     uint32_t* A = P.arena[arena_idx];
     uint32_t* B = P.arena[arena_idx ^ 1];
     const uint32_t tid = block_rank * kBlock + threadIdx.x;
     const uint32_t nthreads = nblocks * kBlock;
-    auto sync = [&]() {
-        if (grid)
-            grid_sync(P.ctl, nblocks);
-        else
-            __syncthreads();
-    };
+    auto sync = [&]() { grid_sync(P.ctl, nblocks, epoch); };
     // phase 1: claim refcount-zero slots and drop their argument references
     // (collect_free_indices, term_store.cpp:140-157); a thread follows the
     // cascade it triggers for a bounded number of hops, the rest waits for
@@ -601,7 +633,6 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, uint32_t& arena_idx, u
 struct Local {
     uint32_t sweep, cur, arena, base;
     unsigned long long total, maxw;
-    long long live;
     uint32_t gc_runs, small_sweeps, last_gc, peak_base;
     unsigned long long gc_ns;
 };
@@ -613,7 +644,6 @@ __device__ void load_local(Local& L, Ctl* c) {
     L.base = ld_cg(&c->base);
     L.total = ld_cg(&c->total_rewrites);
     L.maxw = ld_cg(&c->max_width);
-    L.live = ld_cg(&c->live);
     L.gc_runs = ld_cg(&c->gc_runs);
     L.small_sweeps = ld_cg(&c->small_sweeps);
     L.last_gc = ld_cg(&c->last_gc_sweep);
@@ -628,7 +658,6 @@ __device__ void store_local(const Local& L, Ctl* c) {
     c->base = L.base;
     c->total_rewrites = L.total;
     c->max_width = L.maxw;
-    c->live = L.live;
     c->gc_runs = L.gc_runs;
     c->small_sweeps = L.small_sweeps;
     c->last_gc_sweep = L.last_gc;
@@ -649,7 +678,7 @@ __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32
     // (ensure_headroom, sweep_engine.cpp:290-303)
     const uint64_t worst = (uint64_t)L.base + (uint64_t)m * P.max_new + 1;
     if (worst > P.capacity) {
-        if (P.allow_gc && !just_collected) return kPlanGc;
+        if (P.allow_gc && !just_collected && !P.prefer_grow) return kPlanGc;
         if (!P.fixed_capacity) return kPlanGrow;
         // fixed capacity: go ahead; a claim that does not fit aborts with
         // Capacity like the reference (sweep_engine.cpp:221-226)
@@ -668,7 +697,7 @@ __device__ void record(const Params& P, uint32_t s, unsigned long long width, co
     if (k == 0 || k > P.trace_cap) return;
     trs_gpu_sweep_record r;
     r.sweep = k;
-    r.live_terms = (uint32_t)(L.live < 0 ? 0 : L.live);
+    r.live_terms = L.base - 1;  // allocated and not yet reclaimed by a compaction
     r.rewrites = width;
     r.n = L.base;
     r.free_len = 0;
@@ -678,15 +707,97 @@ __device__ void record(const Params& P, uint32_t s, unsigned long long width, co
     P.trace[k - 1] = r;
 }
 
+// Shared-memory state of the single-CTA mode.
+struct SmallState {
+    uint32_t count[2];    // frontier counts: [cur] being read, [cur^1] being pushed
+    uint32_t alloc;
+    uint32_t abort;       // a claim did not fit the fixed capacity
+    unsigned long long width;
+};
+
+constexpr uint32_t kSmallCap = 4096;  // frontier entries per shared-memory list
+
 template <int W>
-__global__ void __launch_bounds__(kBlock) step_loop(Params P) {
+__device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bool& just_collected,
+                          uint32_t* slist /* 2 * kSmallCap */, SmallState& ss) {
+    Ctl* ctl = P.ctl;
+    const uint32_t s0 = L.sweep + 1;
+    uint32_t m = ld_ctr(&ctl->ctr[s0 & 3]).count;
+    const uint32_t cap_m = kSmallCap / (P.max_new + 1);
+    const uint32_t exit_m = min(P.small_exit, cap_m);
+    if (m > exit_m) return;  // too wide for the shared-memory lists; nothing touched
+    // stage the frontier into shared memory
+    uint32_t* gin = P.list[L.cur];
+    for (uint32_t e = threadIdx.x; e < m; e += kBlock) slist[e] = gin[e];
+    uint32_t sc = 0;  // shared list holding the current frontier
+    if (threadIdx.x == 0) {
+        ss.count[0] = m;
+        ss.abort = 0;
+    }
+    __syncthreads();
+    for (;;) {
+        const uint32_t s = L.sweep + 1;
+        m = ss.count[sc];
+        if (m > exit_m) break;
+        if (plan(P, L, m, just_collected) != kPlanSweep) break;
+        just_collected = false;
+        uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
+        long long cs = (P.profile && threadIdx.x == 0) ? clock64() : 0;
+        __syncthreads();  // everyone has read ss.count[sc]
+        if (threadIdx.x == 0) {
+            ss.count[sc ^ 1] = 0;
+            ss.alloc = 0;
+        }
+        __syncthreads();
+        Acc acc;
+        process_sweep<W>(P, G, sm, P.arena[L.arena], s, m, slist + sc * kSmallCap,
+                         slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], L.base, &ss.alloc, 0, 1, acc,
+                         &ss.abort);
+        unsigned long long rw = block_sum64(acc.rewrites, sm);
+        if (threadIdx.x == 0) ss.width = rw;
+        __syncthreads();
+        const unsigned long long width = ss.width;
+        L.base += ss.alloc;
+        L.peak_base = max(L.peak_base, L.base);
+        L.total += width;
+        L.maxw = width > L.maxw ? width : L.maxw;
+        L.sweep = s;
+        L.small_sweeps++;
+        sc ^= 1;
+        if (threadIdx.x == 0) record(P, s, width, L, m, 1, global_ns() - t0);
+        if (P.profile && threadIdx.x == 0) {
+            for (int k = 0; k < 4; ++k) ctl->prof[k] += acc.t[k];
+            ctl->prof[4] += clock64() - cs;
+            ctl->prof[5] += 1;
+        }
+        if (L.total > P.step_budget) break;
+        if (ss.abort) break;
+    }
+    // hand the frontier back to the grid through the global list
+    m = ss.count[sc];
+    uint32_t* gout = P.list[L.cur];
+    // L.cur is unchanged while the lists live in shared memory
+    for (uint32_t e = threadIdx.x; e < m; e += kBlock) gout[e] = slist[sc * kSmallCap + e];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint32_t s = L.sweep + 1;
+        for (int k = 0; k < 4; ++k) ctl->ctr[k] = SweepCtr{0u, 0u, 0ull};
+        ctl->ctr[s & 3].count = m;
+        store_local(L, ctl);
+    }
+}
+
+template <int W, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ Smem sm;
-    // stage the program tables
+    __shared__ SmallState ss;
+    // stage the program tables; the single-CTA frontier lists follow them
     for (uint32_t o = threadIdx.x * 16; o < P.prog_bytes; o += kBlock * 16)
         *reinterpret_cast<uint4*>(smem_raw + o) = *reinterpret_cast<const uint4*>(P.prog + o);
     __syncthreads();
     const Prog G = view_prog(smem_raw);
+    uint32_t* slist = reinterpret_cast<uint32_t*>(smem_raw + P.prog_bytes);
     const uint32_t nblocks = gridDim.x;
     const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
     Ctl* ctl = P.ctl;
@@ -695,10 +806,32 @@ __global__ void __launch_bounds__(kBlock) step_loop(Params P) {
     load_local(L, ctl);
     bool just_collected = false;
     uint32_t exit_status = kRunning;
+    uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
 
+    if (P.compact_only) {
+        // final compaction: collect until a pass reclaims nothing
+        for (uint32_t round = 0; round < P.compact_only; ++round) {
+            uint32_t before = L.base;
+            const uint32_t s = L.sweep + 1;
+            uint64_t t0 = global_ns();
+            L.base = gc_compact<W>(P, sm, L.arena, L.base, L.cur, ld_ctr(&ctl->ctr[s & 3]).count, blockIdx.x,
+                                   nblocks, G, epoch);
+            L.gc_runs++;
+            L.gc_ns += global_ns() - t0;
+            if (L.base == before) break;
+        }
+        if (leader) {
+            store_local(L, ctl);
+            ctl->status = kDone;
+        }
+        return;
+    }
+
+    // frontier length of the next sweep; read after every barrier that
+    // precedes a sweep (a grid sweep carries it over from its bookkeeping load)
+    uint32_t m = ld_ctr(&ctl->ctr[(L.sweep + 1) & 3]).count;
     for (;;) {
         const uint32_t s = L.sweep + 1;
-        const uint32_t m = ld_cg(&ctl->count[s & 3]);
         const uint32_t pl = plan(P, L, m, just_collected);
         if (pl == kPlanFinish) {
             // the first sweep whose frontier is empty (sweep_engine.cpp:147)
@@ -711,100 +844,57 @@ __global__ void __launch_bounds__(kBlock) step_loop(Params P) {
         if (pl == kPlanGrow) { exit_status = kNeedGrow; break; }
         if (pl == kPlanGc) {
             uint64_t t0 = global_ns();
-            L.base = gc_compact<W>(P, sm, L.arena, L.base, L.cur, m, blockIdx.x, nblocks, G, true);
+            L.base = gc_compact<W>(P, sm, L.arena, L.base, L.cur, m, blockIdx.x, nblocks, G, epoch);
             L.gc_runs++;
             L.last_gc = L.sweep + 1;
             L.gc_ns += global_ns() - t0;
             just_collected = true;
             continue;
         }
-        just_collected = false;
 
         if (m <= P.small_enter) {
-            // ---- single-CTA mode: CTA 0 runs sweeps, the rest of the grid parks
+            // ---- single-CTA mode: CTA 0 runs sweeps out of shared memory,
+            // the rest of the grid parks in the barrier
             const uint32_t before = L.sweep;
-            if (blockIdx.x == 0) {
-                for (;;) {
-                    const uint32_t s2 = L.sweep + 1;
-                    const uint32_t m2 = ld_cg(&ctl->count[s2 & 3]);
-                    if (m2 > P.small_exit) break;
-                    const uint32_t p2 = plan(P, L, m2, just_collected);
-                    if (p2 != kPlanSweep) break;
-                    just_collected = false;
-                    uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
-                    if (threadIdx.x == 0) {
-                        ctl->count[(s2 + 2) & 3] = 0;
-                        ctl->alloc[(s2 + 2) & 3] = 0;
-                        ctl->rew[(s2 + 2) & 3] = 0;
-                        ctl->dead[(s2 + 2) & 3] = 0;
-                    }
-                    Acc acc;
-                    process_sweep<W>(P, G, sm, P.arena[L.arena], s2, m2, P.list[L.cur],
-                                     P.list[L.cur ^ 1], &ctl->count[(s2 + 1) & 3], L.base,
-                                     &ctl->alloc[s2 & 3], 0, 1, acc);
-                    unsigned long long rw = block_sum64(acc.rewrites, sm);
-                    unsigned long long dd = block_sum64(acc.dead, sm);
-                    if (threadIdx.x == 0) {
-                        if (rw) atomicAdd(&ctl->rew[s2 & 3], rw);
-                        if (dd) atomicAdd(&ctl->dead[s2 & 3], dd);
-                    }
-                    __syncthreads();
-                    const unsigned long long width = ld_cg(&ctl->rew[s2 & 3]);
-                    const uint32_t allocd = ld_cg(&ctl->alloc[s2 & 3]);
-                    const unsigned long long died = ld_cg(&ctl->dead[s2 & 3]);
-                    L.base += allocd;
-                    L.peak_base = max(L.peak_base, L.base);
-                    L.live += (long long)allocd - (long long)died;
-                    L.total += width;
-                    L.maxw = width > L.maxw ? width : L.maxw;
-                    L.sweep = s2;
-                    L.cur ^= 1;
-                    L.small_sweeps++;
-                    if (threadIdx.x == 0)
-                        record(P, s2, width, L, m2, 1, global_ns() - t0);
-                    __syncthreads();
-                    if (ld_cg(&ctl->abort_capacity) || L.total > P.step_budget) break;
-                }
-                if (threadIdx.x == 0) store_local(L, ctl);
-            }
-            grid_sync(ctl, nblocks);
+            if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss);
+            grid_sync(ctl, nblocks, epoch, /*park=*/blockIdx.x != 0);
             load_local(L, ctl);
+            m = ld_ctr(&ctl->ctr[(L.sweep + 1) & 3]).count;
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
             if (ld_cg(&ctl->abort_capacity)) { exit_status = kCapacity; break; }
             if (L.total > P.step_budget) { exit_status = kStepBudget; break; }
-            continue;
+            if (L.sweep != before) continue;
+            // no progress in single-CTA mode (frontier too wide for its
+            // lists): fall through to one grid-wide sweep
         }
+        just_collected = false;
 
         // ---- grid-wide sweep
         uint64_t t0 = leader ? global_ns() : 0;
-        if (leader) {
-            ctl->count[(s + 2) & 3] = 0;
-            ctl->alloc[(s + 2) & 3] = 0;
-            ctl->rew[(s + 2) & 3] = 0;
-            ctl->dead[(s + 2) & 3] = 0;
-        }
+        if (leader) ctl->ctr[(s + 2) & 3] = SweepCtr{0u, 0u, 0ull};
         Acc acc;
         process_sweep<W>(P, G, sm, P.arena[L.arena], s, m, P.list[L.cur], P.list[L.cur ^ 1],
-                         &ctl->count[(s + 1) & 3], L.base, &ctl->alloc[s & 3], blockIdx.x,
+                         &ctl->ctr[(s + 1) & 3].count, L.base, &ctl->ctr[s & 3].alloc, blockIdx.x,
                          nblocks, acc);
         unsigned long long rw = block_sum64(acc.rewrites, sm);
-        unsigned long long dd = block_sum64(acc.dead, sm);
-        if (threadIdx.x == 0) {
-            if (rw) atomicAdd(&ctl->rew[s & 3], rw);
-            if (dd) atomicAdd(&ctl->dead[s & 3], dd);
-        }
-        grid_sync(ctl, nblocks);
-        const unsigned long long width = ld_cg(&ctl->rew[s & 3]);
-        const uint32_t allocd = ld_cg(&ctl->alloc[s & 3]);
-        const unsigned long long died = ld_cg(&ctl->dead[s & 3]);
+        if (threadIdx.x == 0 && rw) atomicAdd(&ctl->ctr[s & 3].rew, rw);
+        grid_sync(ctl, nblocks, epoch);
+        const SweepCtr done_ctr = ld_ctr(&ctl->ctr[s & 3]);
+        const SweepCtr next_ctr = ld_ctr(&ctl->ctr[(s + 1) & 3]);
+        const unsigned long long width = done_ctr.rew;
+        const uint32_t allocd = done_ctr.alloc;
+        m = next_ctr.count;
         L.base += allocd;
         L.peak_base = max(L.peak_base, L.base);
-        L.live += (long long)allocd - (long long)died;
         L.total += width;
         L.maxw = width > L.maxw ? width : L.maxw;
         L.sweep = s;
         L.cur ^= 1;
         if (leader) record(P, s, width, L, m, 0, global_ns() - t0);
+        if (P.profile && leader) {
+            for (int k = 0; k < 4; ++k) ctl->prof[k] += acc.t[k];
+            ctl->prof[5] += 1;
+        }
         if (ld_cg(&ctl->abort_capacity)) { exit_status = kCapacity; break; }
         if (L.total > P.step_budget) { exit_status = kStepBudget; break; }
     }
@@ -918,9 +1008,13 @@ struct trs_gpu_engine {
     uint32_t num_symbols = 0;
     std::vector<uint32_t> arity;
     int W = 8;
+    int minb = 1;  // register budget variant of the step loop (see step_loop_for)
 
     // store
-    uint64_t capacity = 0;
+    uint64_t capacity = 0;        // logical capacity (slots) the step loop may use
+    uint64_t alloc_capacity = 0;  // slots physically allocated per arena
+    int alloc_W = 0;
+    uint32_t roots_cap = 0;
     uint32_t* d_arena[2] = {nullptr, nullptr};
     uint32_t* d_list[2] = {nullptr, nullptr};
     uint32_t* d_gcmap = nullptr;
@@ -965,6 +1059,10 @@ void free_store(trs_gpu_engine* e) {
     e->d_ctl = nullptr;
     e->d_trace = nullptr;
     e->loaded = false;
+    e->capacity = e->alloc_capacity = 0;
+    e->alloc_W = 0;
+    e->roots_cap = 0;
+    e->trace_cap = 0;
 }
 
 int words_for_arity(uint32_t max_arity) {
@@ -1124,18 +1222,29 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     return TRS_GPU_OK;
 }
 
-template <int W>
+// Two register budgets per record width: MINB = 1 (no spills, 1 CTA of 512
+// threads per SM) and MINB = 2 (64 registers, 2 CTAs per SM, some spills).
+template <int W, int MINB>
 const void* step_loop_ptr() {
-    return reinterpret_cast<const void*>(&step_loop<W>);
+    return reinterpret_cast<const void*>(&step_loop<W, MINB>);
 }
 
-const void* step_loop_for(int W) {
+const void* step_loop_for(int W, int minb) {
+    if (minb >= 2) {
+        switch (W) {
+            case 8: return step_loop_ptr<8, 2>();
+            case 16: return step_loop_ptr<16, 2>();
+            default: return step_loop_ptr<32, 2>();
+        }
+    }
     switch (W) {
-        case 8: return step_loop_ptr<8>();
-        case 16: return step_loop_ptr<16>();
-        default: return step_loop_ptr<32>();
+        case 8: return step_loop_ptr<8, 1>();
+        case 16: return step_loop_ptr<16, 1>();
+        default: return step_loop_ptr<32, 1>();
     }
 }
+
+size_t dyn_smem(const trs_gpu_engine* e) { return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t); }
 
 int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     size_t rec_bytes = (size_t)e->W * 4;
@@ -1145,14 +1254,17 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     }
     CUDA_TRY(e, cudaMalloc(&e->d_gcmap, sizeof(uint32_t) * capacity));
     e->capacity = capacity;
+    e->alloc_capacity = capacity;
+    e->alloc_W = e->W;
     return TRS_GPU_OK;
 }
 
 int grid_blocks(trs_gpu_engine* e, uint32_t blocks_per_sm) {
     int occ = 0;
-    size_t dyn = e->blob.size();
-    cudaFuncSetAttribute(step_loop_for(e->W), cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, step_loop_for(e->W), kBlock, dyn) != cudaSuccess || occ < 1)
+    size_t dyn = dyn_smem(e);
+    const void* fn = step_loop_for(e->W, e->minb);
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, dyn) != cudaSuccess || occ < 1)
         occ = 1;
     if (blocks_per_sm) occ = std::min<int>(occ, (int)blocks_per_sm);
     return occ * e->sm_count;
@@ -1167,6 +1279,10 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     uint64_t cap = std::max<uint64_t>(needed, e->capacity * 2);
     if (cap > 0xFFFFFFF0ull) cap = 0xFFFFFFF0ull;
     if (cap <= e->capacity) return fail(e, TRS_GPU_CAPACITY, "term store would exceed 2^32 slots");
+    if (cap <= e->alloc_capacity) {
+        e->capacity = cap;
+        return TRS_GPU_OK;
+    }
     size_t rec_bytes = (size_t)e->W * 4;
     uint32_t* na[2] = {nullptr, nullptr};
     uint32_t* nl[2] = {nullptr, nullptr};
@@ -1184,8 +1300,7 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
         return fail(e, TRS_GPU_CAPACITY, "device memory exhausted while growing the term store");
     }
     uint32_t s = c.sweep + 1;
-    uint32_t m = 0;
-    std::memcpy(&m, &c.count[s & 3], sizeof(m));
+    uint32_t m = c.ctr[s & 3].count;
     CUDA_TRY(e, cudaMemcpyAsync(na[c.arena], e->d_arena[c.arena], rec_bytes * c.base, cudaMemcpyDeviceToDevice, e->stream));
     CUDA_TRY(e, cudaMemcpyAsync(nl[c.cur], e->d_list[c.cur], sizeof(uint32_t) * m, cudaMemcpyDeviceToDevice, e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
@@ -1198,7 +1313,26 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     cudaFree(e->d_gcmap);
     e->d_gcmap = nm;
     e->capacity = cap;
+    e->alloc_capacity = cap;
     return TRS_GPU_OK;
+}
+
+void reset_barrier(trs_gpu_engine* e) {
+    cudaMemsetAsync(reinterpret_cast<uint8_t*>(e->d_ctl) + offsetof(Ctl, bar_arrive), 0, sizeof(uint32_t), e->stream);
+}
+
+// Growing is preferred over collecting while the twin arenas, lists and
+// map of the grown store fit comfortably in free HBM; the compacting GC is
+// the memory-pressure path (and what fixed-capacity stores rely on).
+bool prefer_grow(trs_gpu_engine* e) {
+    size_t free_b = 0, total_b = 0;
+    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    uint64_t next = e->capacity * 2;
+    uint64_t need = next * ((uint64_t)e->W * 4 * 2 + 4 * 3);
+    return need < free_b / 2;
 }
 
 int grow_trace(trs_gpu_engine* e) {
@@ -1232,24 +1366,36 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     if (capacity != 0 && capacity < n)
         return fail(e, TRS_GPU_CAPACITY, "store capacity " + std::to_string(capacity) + " cannot hold " +
                                              std::to_string(n - 1) + " input term nodes");
-    free_store(e);
-    if (capacity == 0) {
+    uint64_t want = capacity;
+    if (want == 0) {
         // auto: room for the input and a generous allocation window; the
         // step loop collects and grows on demand
-        capacity = std::max<uint64_t>((uint64_t)n * 4 + 1024, 1ull << 22);
+        want = std::max<uint64_t>((uint64_t)n * 4 + 1024, 1ull << 22);
+        if (e->alloc_W == e->W && e->alloc_capacity > want) want = e->alloc_capacity;
     }
-    int rc = alloc_store(e, capacity);
-    if (rc) return rc;
-    CUDA_TRY(e, cudaMalloc(&e->d_ctl, sizeof(Ctl)));
+    if (e->alloc_W != e->W || e->alloc_capacity < want) {
+        free_store(e);
+        int rc = alloc_store(e, want);
+        if (rc) return rc;
+    }
+    e->capacity = want;
+    if (!e->d_ctl) CUDA_TRY(e, cudaMalloc(&e->d_ctl, sizeof(Ctl)));
     CUDA_TRY(e, cudaMemsetAsync(e->d_ctl, 0, sizeof(Ctl), e->stream));
-    CUDA_TRY(e, cudaMalloc(&e->d_roots, sizeof(uint32_t) * num_roots));
+    if (e->roots_cap < num_roots) {
+        cudaFree(e->d_roots);
+        CUDA_TRY(e, cudaMalloc(&e->d_roots, sizeof(uint32_t) * num_roots));
+        e->roots_cap = num_roots;
+    }
     CUDA_TRY(e, cudaMemcpyAsync(e->d_roots, roots, sizeof(uint32_t) * num_roots, cudaMemcpyHostToDevice, e->stream));
-    CUDA_TRY(e, cudaMalloc(&e->d_blocksum, sizeof(uint32_t) * (e->sm_count * 32 + 1)));
-    e->trace_cap = 1u << 16;
-    CUDA_TRY(e, cudaMalloc(&e->d_trace, sizeof(trs_gpu_sweep_record) * e->trace_cap));
+    if (!e->d_blocksum) CUDA_TRY(e, cudaMalloc(&e->d_blocksum, sizeof(uint32_t) * (e->sm_count * 32 + 1)));
+    if (!e->d_trace) {
+        e->trace_cap = 1u << 16;
+        CUDA_TRY(e, cudaMalloc(&e->d_trace, sizeof(trs_gpu_sweep_record) * e->trace_cap));
+    }
     if (e->d_prog == nullptr) return fail(e, TRS_GPU_INVALID, "program not staged");
-    // frontier count of sweep 1 lives in ctl->count[1]
-    uint32_t* d_count = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(e->d_ctl) + offsetof(Ctl, count)) + 1;
+    // frontier count of sweep 1 lives in ctl->ctr[1].count
+    uint32_t* d_count = reinterpret_cast<uint32_t*>(reinterpret_cast<uint8_t*>(e->d_ctl) + offsetof(Ctl, ctr) +
+                                                    sizeof(SweepCtr) * 1 + offsetof(SweepCtr, count));
     const uint8_t* d_arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
     cudaEvent_t a, b;
     cudaEventCreate(&a);
@@ -1273,8 +1419,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     cudaEventDestroy(b);
     uint32_t count1 = 0;
     CUDA_TRY(e, cudaMemcpy(&count1, d_count, sizeof(uint32_t), cudaMemcpyDeviceToHost));
-    init.count[1] = count1;
-    init.live = n - 1;  // corrected below for unreferenced input slots (rare)
+    init.ctr[1].count = count1;
     CUDA_TRY(e, cudaMemcpy(e->d_ctl, &init, sizeof(Ctl), cudaMemcpyHostToDevice));
     e->num_roots = num_roots;
     e->loaded = true;
@@ -1408,7 +1553,9 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     trs_gpu_options opt{};
     if (opt_in) opt = *opt_in;
     e->last_error.clear();
-    const int blocks = grid_blocks(e, opt.blocks_per_sm);
+    e->minb = opt.variant == 2 ? 2 : 1;
+    int blocks = grid_blocks(e, opt.blocks_per_sm);
+    if (opt.max_blocks && (int)opt.max_blocks < blocks) blocks = (int)opt.max_blocks;
     trs_gpu_stats st{};
     st.grid_blocks = blocks;
     st.block_threads = kBlock;
@@ -1458,9 +1605,13 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         P.fixed_capacity = opt.fixed_capacity;
         P.max_new = e->max_new;
         P.sweep0 = sweep0;
+        P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
+        P.profile = opt.profile;
         void* args[] = {&P};
         cudaEventRecord(a, e->stream);
-        cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W), blocks, kBlock, args, e->blob.size(), e->stream);
+        reset_barrier(e);
+        reset_barrier(e);
+    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
         cudaEventRecord(b, e->stream);
         st.launches++;
         if (err != cudaSuccess) {
@@ -1500,7 +1651,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         }
         if (c.status == kNeedGrow) {
             uint32_t s = c.sweep + 1;
-            uint64_t m = c.count[s & 3];
+            uint64_t m = c.ctr[s & 3].count;
             st.regrows++;
             int r = grow_store(e, (uint64_t)c.base + m * e->max_new + 1 + (1u << 20));
             if (r) { result = r; break; }
@@ -1519,7 +1670,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     st.gc_runs = c.gc_runs;
     st.small_sweeps = c.small_sweeps;
     st.peak_slots = c.peak_base;
-    st.live_terms = c.live < 0 ? 0 : (uint64_t)c.live;
+    st.live_terms = c.base - 1;
     st.kernel_ms = total_ms;
     st.gc_ms = c.gc_ns * 1e-6;
     st.load_ms = e->load_ms;
@@ -1554,6 +1705,90 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     }
     if (stats) *stats = st;
     return result;
+}
+
+void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr; }
+
+int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out6) {
+    if (!e || !e->d_ctl || !out6) return TRS_GPU_INVALID;
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    for (int k = 0; k < 6; ++k) out6[k] = c.prof[k];
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats) {
+    if (!e || !e->loaded) return TRS_GPU_INVALID;
+    cudaSetDevice(e->device);
+    Ctl c0;
+    CUDA_TRY(e, cudaMemcpy(&c0, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    Params P{};
+    P.arena[0] = e->d_arena[0];
+    P.arena[1] = e->d_arena[1];
+    P.list[0] = e->d_list[0];
+    P.list[1] = e->d_list[1];
+    P.gcmap = e->d_gcmap;
+    P.blocksum = e->d_blocksum;
+    P.roots = e->d_roots;
+    P.num_roots = e->num_roots;
+    P.ctl = e->d_ctl;
+    P.trace = e->d_trace;
+    P.trace_cap = e->trace_cap;
+    P.prog = e->d_prog;
+    P.prog_bytes = (uint32_t)e->blob.size();
+    P.capacity = e->capacity;
+    P.max_new = e->max_new;
+    P.sweep0 = c0.sweep;
+    P.allow_gc = 1;
+    P.compact_only = max_rounds ? max_rounds : 8;
+    const int blocks = grid_blocks(e, 0);
+    void* args[] = {&P};
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    cudaEventRecord(a, e->stream);
+    reset_barrier(e);
+    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
+    cudaEventRecord(b, e->stream);
+    if (err == cudaSuccess) err = cudaEventSynchronize(b);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("compaction: ") + cudaGetErrorString(err));
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    if (stats) {
+        std::memset(stats, 0, sizeof(*stats));
+        stats->gc_runs = c.gc_runs - c0.gc_runs;
+        stats->gc_ms = (c.gc_ns - c0.gc_ns) * 1e-6;
+        stats->kernel_ms = ms;
+        stats->launches = 1;
+        stats->live_terms = c.base - 1;
+        stats->peak_slots = c.base;
+        stats->grid_blocks = blocks;
+        stats->block_threads = kBlock;
+        stats->record_words = e->W;
+    }
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_fetch_records(trs_gpu_engine* e, void* dst, uint64_t cap_bytes, uint64_t* bytes, uint32_t* record_words,
+                          uint32_t* roots_out) {
+    if (!e || !e->loaded) return TRS_GPU_INVALID;
+    cudaSetDevice(e->device);
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    uint64_t need = (uint64_t)c.base * e->W * 4;
+    if (bytes) *bytes = need;
+    if (record_words) *record_words = (uint32_t)e->W;
+    if (!dst || cap_bytes < need) return TRS_GPU_OK;
+    CUDA_TRY(e, cudaMemcpyAsync(dst, e->d_arena[c.arena], need, cudaMemcpyDeviceToHost, e->stream));
+    if (roots_out)
+        CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    return TRS_GPU_OK;
 }
 
 int trs_gpu_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count) {

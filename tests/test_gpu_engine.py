@@ -1,0 +1,213 @@
+"""GPU engine behaviour through the C ABI: error model, batched roots,
+device knobs that must not change results, and the full-size BASELINE
+configs (bit-exact against reference-derived fixtures)."""
+import hashlib
+import json
+import os
+
+import numpy as np
+import pytest
+
+from paper_2009_07174_b200 import api
+from paper_2009_07174_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(__file__)
+CASES = json.load(open(os.path.join(HERE, "golden", "small.json")))["cases"]
+COUNTS = json.load(open(os.path.join(HERE, "golden", "workload_counts.json")))
+
+
+def run(engine, texts, **opts):
+    return api.normalize_texts(texts, engine=engine, options=api.make_options(**opts))
+
+
+def test_step_budget_raises(engine):
+    # sweep_engine_tests.cpp:223-236
+    text = "sort T = A() | F(T);\nvar X : T;\neqn F(X) = F(F(X));\ninput F(A());\n"
+    with pytest.raises(api.EngineError) as ei:
+        run(engine, text, step_budget=500)
+    assert ei.value.fault == api.EngineFault.StepBudget
+
+
+def test_fixed_capacity_fails_hard(engine):
+    # sweep_engine_tests.cpp:203-210 (load capacity 64 with growth disabled)
+    s = api.System(W.mergesort(20, 4))
+    st = api.Store.load(s)
+    engine.set_program(s)
+    engine.load(st, capacity=st.view()["n"] + 8)
+    with pytest.raises(api.EngineError) as ei:
+        engine.run(api.make_options(fixed_capacity=1, disable_gc=1))
+    assert ei.value.fault == api.EngineFault.Capacity
+
+
+def test_fixed_capacity_with_gc_recycles(engine):
+    """A tight fixed arena still completes when compaction can reclaim garbage."""
+    g = CASES["mergesort64_s1"]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    engine.set_program(s)
+    engine.load(st)
+    peak = engine.run(api.make_options(disable_gc=1))["peak_slots"]
+    collected = 0
+    for frac in (0.8, 0.6, 0.5):
+        engine.load(st, capacity=int(peak * frac))
+        stats = engine.run(api.make_options(fixed_capacity=1, validate=1))
+        assert stats["total_rewrites"] == g["rewrites"]
+        np.testing.assert_array_equal(engine.trace()["rewrites"], np.asarray(g["widths"], np.uint64))
+        np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
+        collected += stats["gc_runs"]
+    assert collected > 0
+
+
+def test_growth_is_invisible(engine):
+    # sweep_engine_tests.cpp:212-221: a tiny initial arena grows on demand
+    g = CASES["treemergesort_4_5_s7"]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    engine.set_program(s)
+    engine.load(st, capacity=st.view()["n"] + 1)
+    stats = engine.run(api.make_options(disable_gc=1))
+    assert stats["regrows"] > 0 and stats["total_rewrites"] == g["rewrites"]
+    np.testing.assert_array_equal(engine.trace()["rewrites"], np.asarray(g["widths"], np.uint64))
+
+
+def test_explicit_capacity_below_input_fails(engine):
+    s = api.System(W.fib(5))
+    st = api.Store.load(s)
+    engine.set_program(s)
+    with pytest.raises(api.EngineError):
+        engine.load(st, capacity=2)
+
+
+def test_dangling_reference_detected(engine):
+    s = api.System(W.mergesort(2).split("input ")[0] + "input Cons(Zero(), Cons(Zero(), Nil()));\n")
+    st = api.Store.load(s)
+    st.poke_arg(1, 1, 0)  # Cons's tail -> slot 0
+    engine.set_program(s)
+    engine.load(st)
+    engine.run()
+    with pytest.raises(api.EngineError) as ei:
+        engine.canonical(0)
+    assert ei.value.fault == api.EngineFault.DanglingReference
+
+
+def test_batched_roots_equal_individual_runs(engine):
+    # one store, three independent roots (same signature): fib-batch shards
+    texts = [W.fib_batch(s, roots=16) for s in (1, 2, 3)]
+    res = run(engine, texts)
+    total = 0
+    widths = None
+    for k, t in enumerate(texts):
+        one = run(engine, t)
+        np.testing.assert_array_equal(res.words[k], one.words[0])
+        total += one.total_rewrites
+        w = one.widths
+        widths = w if widths is None else _pad_add(widths, w)
+    assert res.total_rewrites == total
+    np.testing.assert_array_equal(res.widths, widths)  # independent roots: widths add per sweep
+
+
+def _pad_add(a, b):
+    n = max(len(a), len(b))
+    out = np.zeros(n, np.uint64)
+    out[: len(a)] += a
+    out[: len(b)] += b
+    return out
+
+
+@pytest.mark.parametrize("opts", [dict(variant=2), dict(max_blocks=1), dict(small_enter=1 << 20, small_exit=1 << 20),
+                                  dict(disable_small=1, gc_interval=3), dict(blocks_per_sm=1, small_enter=4)])
+@pytest.mark.parametrize("name", ["treemergesort_4_5_s7", "fibbatch64_s3", "unit_two_waiters", "transform6"])
+def test_knobs_do_not_change_results(engine, name, opts):
+    g = CASES[name]
+    res = run(engine, g["text"], **opts)
+    assert res.total_rewrites == g["rewrites"]
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+
+
+def test_rerun_after_normal_form(engine):
+    """A second run on an already-normal store: one empty sweep, zero rewrites."""
+    s = api.System(CASES["fib10"]["text"])
+    engine.set_program(s)
+    engine.load(api.Store.load(s))
+    engine.run()
+    st = engine.run()
+    assert st["total_rewrites"] == 0 and st["sweeps"] == 1
+
+
+def test_compact_and_fetch(engine):
+    g = CASES["fibbatch64_s3"]
+    s = api.System(g["text"])
+    engine.set_program(s)
+    engine.load(api.Store.load(s))
+    engine.run()
+    c = engine.compact(8)
+    nbytes, words = engine.fetch_records()
+    assert words == 8 and nbytes == (c["live_terms"] + 1) * 32
+    np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
+    assert c["live_terms"] + 1 <= g["nodes"] + 2
+
+
+def test_trace_records(engine):
+    # sweep_engine_tests.cpp:238-255
+    res = run(engine, CASES["mergesort10_s3"]["text"])
+    tr = res.trace
+    assert list(tr["sweep"]) == list(range(1, len(tr) + 1))
+    assert (tr["n"] >= 2).all() and (tr["live_terms"] >= 1).all()
+    assert tr["rewrites"].max() <= res.total_rewrites
+
+
+def _sha(widths):
+    return hashlib.sha1(np.asarray(widths, "<u8").tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name", ["fib18", "transform22", "reverse16k", "ackermann36", "buildsum22"])
+def test_full_size_config_widths(engine, name):
+    """Full BASELINE sizes: rewrites, sweeps and the per-sweep width vector
+    (sha1) equal the reference-derived fixture."""
+    c = COUNTS.get(name)
+    if c is None:
+        pytest.skip(f"{name} not in workload_counts.json")
+    res = run(engine, W.CONFIGS[name][0](), )
+    assert res.total_rewrites == c["rewrites"] and res.sweeps == c["sweeps"]
+    assert _sha(res.widths) == c["widths_sha1"]
+
+
+def test_full_size_normal_forms(engine):
+    """Size-independent properties of the full configs' normal forms."""
+    s = api.System(W.fib(18))
+    res = run(engine, W.fib(18))
+    assert s.print_words(res.words[0]) == W.peano(2584)  # Fib(18) = 2584
+    res = run(engine, W.ackermann(3, 6))
+    assert api.System(W.ackermann(3, 6)).print_words(res.words[0]) == W.peano(509)
+    res = run(engine, W.buildsum(22))
+    assert res.total_rewrites == 33_554_404 and res.sweeps == 689
+    assert api.System(W.buildsum(22)).print_words(res.words[0]) == "B0(" * 22 + "B1(Z())" + ")" * 22
+    res = run(engine, W.transform(22))
+    assert res.total_rewrites == (2 ** 23 - 1) + 26 * 2 ** 22  # seq_engine_tests.cpp:39-43
+    words = res.words[0]
+    assert len(words) == 3 * (2 ** 22 - 1) + 2 ** 22  # full binary tree of End leaves, no sharing
+
+
+def test_full_size_mergesort_sorts(engine):
+    """mergesort(2^14): the normal form is the independently sorted list."""
+    text = W.mergesort(16384, 1)
+    s = api.System(text)
+    res = run(engine, text)
+    assert res.total_rewrites == 4_538_513 and res.sweeps == 818_968
+    nums = sorted(W.generated_numerals("mergesort", 16384, seed=1))
+    expect = "".join(f"Cons({W.peano(v)}, " for v in nums) + "Nil()" + ")" * len(nums)
+    assert s.print_words(res.words[0]) == expect
+
+
+def test_full_size_batch_shard(engine):
+    c = COUNTS["fibbatch_s1"]
+    res = run(engine, W.fib_batch(1))
+    assert res.total_rewrites == c["rewrites"] and res.sweeps == c["sweeps"]
+    assert _sha(res.widths) == c["widths_sha1"]
+    c = COUNTS["sortbatch_s1"]
+    res = run(engine, W.treemergesort_batch(1))
+    assert res.total_rewrites == c["rewrites"] and res.sweeps == c["sweeps"]
+    assert _sha(res.widths) == c["widths_sha1"]

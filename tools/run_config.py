@@ -41,6 +41,11 @@ def main():
     ap.add_argument("--small-exit", type=int, default=0)
     ap.add_argument("--gc-interval", type=int, default=0)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--trace-out", default="")
+    ap.add_argument("--max-blocks", type=int, default=0)
+    ap.add_argument("--profile", action="store_true")
     args = ap.parse_args()
     texts = texts_for(args.name)
     t0 = time.time()
@@ -49,7 +54,9 @@ def main():
     t1 = time.time()
     eng = api.Engine(0)
     opts = api.make_options(disable_small=int(args.disable_small), small_enter=args.small_enter,
-                            small_exit=args.small_exit, gc_interval=args.gc_interval)
+                            small_exit=args.small_exit, gc_interval=args.gc_interval, variant=args.variant,
+                            blocks_per_sm=args.blocks_per_sm, max_blocks=args.max_blocks,
+                            profile=int(args.profile))
     for rep in range(args.reps):
         res = eng.normalize(systems[0], store, opts, words=(rep == args.reps - 1))
         st = res.stats
@@ -62,6 +69,13 @@ def main():
                           "grid": st["grid_blocks"], "regrows": st["regrows"], "load_ms": st["load_ms"]}),
               flush=True)
     print(f"parse+load host {t1 - t0:.2f}s", flush=True)
+    if args.profile:
+        pc = eng.profile_counters()
+        n = max(1, pc["sweeps"])
+        print(json.dumps({"cycles_per_sweep": {k: pc[k] / n for k in ("match", "claim", "apply", "push", "sweep")},
+                          "profiled_sweeps": pc["sweeps"]}), flush=True)
+    if args.trace_out:
+        np.save(args.trace_out, res.trace)
     if args.ref:
         from oracle import ref
         for k, t in enumerate(texts[:1]):
