@@ -116,7 +116,8 @@ typedef struct trs_gpu_options {
     uint32_t variant;          /* step-loop register budget: 0/1 = 1 CTA/SM no spills, 2 = 2 CTAs/SM */
     uint32_t max_blocks;       /* >0: cap the persistent grid (profiling the single-CTA mode) */
     uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters) */
-    uint32_t reserved[5];
+    uint32_t disable_warp_mode; /* 1: frontiers <= 32 slots still run on the whole CTA */
+    uint32_t reserved[4];
 } trs_gpu_options;
 
 /* Per-sweep record (reference SweepRecord, sweep_engine.hpp:10-17).

@@ -62,7 +62,8 @@ class Options(ctypes.Structure):
         ("variant", ctypes.c_uint32),
         ("max_blocks", ctypes.c_uint32),
         ("profile", ctypes.c_uint32),
-        ("reserved", ctypes.c_uint32 * 5),
+        ("disable_warp_mode", ctypes.c_uint32),
+        ("reserved", ctypes.c_uint32 * 4),
     ]
 
 

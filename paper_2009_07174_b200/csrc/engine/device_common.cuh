@@ -1,0 +1,268 @@
+// Device-side building blocks shared by the step loop and the collector:
+// control block, launch parameters, grid barrier, block scans, record access.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device_program.hpp"
+#include "trs_gpu.h"
+
+namespace trs_b200 {
+
+constexpr int kBlock = 512;
+constexpr int kWarps = kBlock / 32;
+constexpr uint32_t kMaxGrid = 1024;    // CTAs; sizes the frontier region tables
+constexpr uint32_t kSmallCap = 4096;   // frontier entries per shared-memory list (single-CTA mode)
+
+enum Status : uint32_t {
+    kRunning = 0,
+    kDone = 1,
+    kStepBudget = 2,
+    kCapacity = 3,
+    kNeedGrow = 4,
+    kNeedTrace = 5,
+};
+
+// Control block in device memory.  Persistent fields are written by one
+// thread at quiescent points only (kernel exit, single-CTA hand-back, end of
+// a collection); every CTA keeps an identical private copy (Local) in
+// between, so no CTA ever needs a fresh read of shared bookkeeping to decide
+// what the grid does next.
+struct Ctl {
+    uint32_t sweep;           // completed sweeps
+    uint32_t cur;             // frontier list buffer of the next sweep
+    uint32_t arena;           // current arena buffer
+    uint32_t status;
+    uint32_t gc_runs;
+    uint32_t small_sweeps;
+    uint32_t last_gc_sweep;
+    uint32_t abort_capacity;  // a claim did not fit a fixed capacity
+    unsigned long long total_rewrites;
+    unsigned long long max_width;
+    unsigned long long gc_ns;
+    uint32_t peak_bump;
+    uint32_t pad0;
+    // allocator: slots [0, bump) are handed out (in per-warp slabs)
+    uint32_t bump;
+    // grid barrier: monotonic arrival counter, zeroed by the host per launch
+    uint32_t bar_arrive;
+    // frontier layout: list buffer b holds nregions[b] regions whose
+    // (offset, count) pairs live in Params::regions
+    uint32_t nregions[2];
+    // phase cycle accounting (Params::profile): match, claim, apply, push, sweep, sweeps
+    unsigned long long prof[6];
+};
+
+struct Params {
+    uint32_t* arena[2];
+    uint32_t* list[2];
+    uint32_t* gcmap;
+    uint32_t* blocksum;
+    uint32_t* regions;               // [2 buffers][off | cnt][kMaxGrid]
+    unsigned long long* region_rew;  // [2 buffers][kMaxGrid] rewrites of the sweep that wrote the buffer
+    uint32_t* roots;
+    uint32_t num_roots;
+    Ctl* ctl;
+    trs_gpu_sweep_record* trace;
+    uint32_t trace_cap;
+    const uint8_t* prog;  // blob in global memory
+    uint32_t prog_bytes;
+    uint64_t capacity;  // logical slots per arena
+    uint64_t step_budget;
+    uint32_t small_enter, small_exit;
+    uint32_t warp_mode;  // tiny frontiers run on one warp
+    uint32_t gc_interval;
+    uint32_t allow_gc;
+    uint32_t fixed_capacity;
+    uint32_t max_new;
+    uint32_t sweep0;        // sweeps completed before this run (epochs keep counting)
+    uint32_t compact_only;  // >0: run at most this many compaction rounds and exit
+    uint32_t prefer_grow;   // out of headroom: grow (host) rather than collect
+    uint32_t profile;       // phase cycle accounting of CTA 0 (debug)
+    uint32_t slab;          // fresh slots a warp claims at a time
+};
+
+__device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {
+    return P.regions + buf * 2 * kMaxGrid;
+}
+__device__ __forceinline__ uint32_t* region_cnt(const Params& P, uint32_t buf) {
+    return P.regions + buf * 2 * kMaxGrid + kMaxGrid;
+}
+
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void red_release_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Software grid barrier (all CTAs are co-resident: cooperative launch).
+// Arrivals are fire-and-forget increments of one monotonic counter; the
+// k-th barrier completes when it reaches k * nblocks, so nobody resets it.
+// `park` is for CTAs idling while CTA 0 runs single-CTA sweeps: they back
+// off to microsecond sleeps so their polling does not load the L2 slice
+// CTA 0 is working against.
+__device__ __forceinline__ void grid_sync(Ctl* ctl, uint32_t nblocks, uint32_t& epoch, bool park = false) {
+    __syncthreads();
+    ++epoch;
+    if (threadIdx.x == 0) {
+        red_release_add(&ctl->bar_arrive, 1u);
+        const uint32_t target = epoch * nblocks;
+        uint32_t ns = 32;
+        while ((int)(ld_acquire(&ctl->bar_arrive) - target) < 0) {
+            __nanosleep(ns);
+            if (park && ns < 4096) ns <<= 1;
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+struct Smem {
+    uint32_t scan[kWarps];
+    uint32_t bcast[4];
+    unsigned long long red[kWarps];
+};
+
+// Exclusive block scan of v; *total gets the block sum.  Ends synchronised.
+__device__ __forceinline__ uint32_t block_scan(uint32_t v, uint32_t* total, Smem& sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sm.scan[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+        uint32_t w = lane < kWarps ? sm.scan[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kWarps) sm.scan[lane] = w;
+    }
+    __syncthreads();
+    uint32_t prefix = warp > 0 ? sm.scan[warp - 1] : 0;
+    *total = sm.scan[kWarps - 1];
+    __syncthreads();
+    return prefix + x - v;
+}
+
+// Block-wide sum, valid in every thread.  Ends synchronised.
+__device__ __forceinline__ unsigned long long block_sum64(unsigned long long v, Smem& sm) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sm.red[warp] = v;
+    __syncthreads();
+    unsigned long long t = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) t += sm.red[w];
+    __syncthreads();
+    return t;
+}
+
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    return x;
+}
+
+// Typed views of the program blob staged in shared memory.
+struct Prog {
+    const uint8_t* arity;
+    const uint16_t* rule_begin;
+    const DRule* rules;
+    const DStep* steps;
+    const DInstr* instrs;
+    const uint16_t* refs;
+    uint32_t max_new;
+};
+
+__device__ __forceinline__ Prog view_prog(const uint8_t* blob) {
+    const ProgHeader* h = reinterpret_cast<const ProgHeader*>(blob);
+    Prog p;
+    p.arity = blob + h->off_arity;
+    p.rule_begin = reinterpret_cast<const uint16_t*>(blob + h->off_rule_begin);
+    p.rules = reinterpret_cast<const DRule*>(blob + h->off_rules);
+    p.steps = reinterpret_cast<const DStep*>(blob + h->off_steps);
+    p.instrs = reinterpret_cast<const DInstr*>(blob + h->off_instrs);
+    p.refs = reinterpret_cast<const uint16_t*>(blob + h->off_refs);
+    p.max_new = h->max_new_slots;
+    return p;
+}
+
+template <int N>
+__device__ __forceinline__ uint32_t pick(const uint32_t (&v)[N], uint32_t k) {
+    uint32_t r = v[0];
+#pragma unroll
+    for (int t = 1; t < N; ++t)
+        if (k == (uint32_t)t) r = v[t];
+    return r;
+}
+
+template <int W>
+__device__ __forceinline__ uint32_t* rec(uint32_t* arena, uint32_t i) {
+    return arena + (size_t)i * W;
+}
+
+// Load the first `ar` argument words of a record (whole 16-byte quads).
+template <int W>
+__device__ __forceinline__ void load_args(const uint32_t* r, uint32_t ar, uint32_t (&a)[W - 4]) {
+#pragma unroll
+    for (int q = 0; q < (W - 4) / 4; ++q) {
+        if ((uint32_t)(q * 4) < ar) {
+            uint4 v = *reinterpret_cast<const uint4*>(r + kWArgs + q * 4);
+            a[q * 4 + 0] = v.x;
+            a[q * 4 + 1] = v.y;
+            a[q * 4 + 2] = v.z;
+            a[q * 4 + 3] = v.w;
+        } else {
+            a[q * 4 + 0] = a[q * 4 + 1] = a[q * 4 + 2] = a[q * 4 + 3] = 0;
+        }
+    }
+}
+
+template <int W>
+__device__ __forceinline__ void store_args(uint32_t* r, const uint32_t (&a)[W - 4], uint32_t ar) {
+#pragma unroll
+    for (int q = 0; q < (W - 4) / 4; ++q) {
+        if ((uint32_t)(q * 4) < ar || q == 0) {
+            *reinterpret_cast<uint4*>(r + kWArgs + q * 4) =
+                make_uint4(a[q * 4 + 0], a[q * 4 + 1], a[q * 4 + 2], a[q * 4 + 3]);
+        }
+    }
+}
+
+// Entries of a sweep are handed out in 32-entry chunks round-robin over all
+// warps of the participating CTAs, so CTA b of n processes exactly
+// cta_entries(b) of m entries and the entries of CTAs < b number
+// cta_prefix(b); its next-frontier pushes (at most max_new + 1 per entry)
+// therefore fit the output region [(max_new+1) * prefix, +(max_new+1) * count).
+__device__ __forceinline__ uint32_t cta_prefix(uint32_t m, uint32_t b, uint32_t nblocks) {
+    const uint64_t round = (uint64_t)nblocks * kBlock;
+    const uint64_t full = m / round;
+    const uint64_t rem = m - full * round;
+    const uint64_t before = (uint64_t)b * kBlock;
+    return (uint32_t)(full * before + (rem < before ? rem : before));
+}
+
+}  // namespace trs_b200

@@ -1,0 +1,143 @@
+// Compacting garbage collector (grid-wide, inside the persistent step loop).
+//
+// Counterpart of the reference's collect_free_indices (term_store.cpp:140-157)
+// plus its free ring, re-designed for bump allocation: refcount-zero slots
+// are claimed (head := dead) and drop their argument references; then the
+// live slots are stream-compacted, in order, into the twin arena with block
+// scans and a grid-wide prefix over per-CTA counts, and an old -> new index
+// map is applied to every argument, waiter word, frontier entry and root.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace trs_b200 {
+
+// Frontier list of one sweep: R regions of a list buffer, with their
+// exclusive prefix over counts staged in shared memory.
+struct Frontier {
+    uint32_t R;
+    uint32_t M;
+    const uint32_t* pref;  // [R + 1], pref[R] = M
+    const uint32_t* off;   // [R]
+};
+
+__device__ __forceinline__ uint32_t frontier_phys(const Frontier& f, uint32_t v) {
+    if (f.R == 1) return f.off[0] + v;
+    uint32_t lo = 0, hi = f.R - 1;  // largest r with pref[r] <= v
+    while (lo < hi) {
+        uint32_t mid = (lo + hi + 1) >> 1;
+        if (f.pref[mid] <= v)
+            lo = mid;
+        else
+            hi = mid - 1;
+    }
+    return f.off[lo] + (v - f.pref[lo]);
+}
+
+// Returns the new bump pointer.  The caller has staged `in` (regions of
+// list buffer `cur`) and abandoned every warp's slab; on return the
+// frontier is one dense region of buffer cur ^ 1 and arena_idx is flipped.
+template <int W>
+__device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_t& arena_idx, uint32_t bump,
+                               const Frontier& in, uint32_t cur, uint32_t block_rank, uint32_t nblocks,
+                               uint32_t& epoch) {
+    uint32_t* A = P.arena[arena_idx];
+    uint32_t* B = P.arena[arena_idx ^ 1];
+    const uint32_t tid = block_rank * kBlock + threadIdx.x;
+    const uint32_t nthreads = nblocks * kBlock;
+    // phase 1: claim refcount-zero slots and drop their argument references.
+    // A thread follows the cascade it triggers for a bounded number of hops;
+    // the rest waits for a later collection, as the reference defers it.
+    for (uint32_t x = 1 + tid; x < bump; x += nthreads) {
+        uint32_t* R = rec<W>(A, x);
+        uint32_t head = __ldcg(R + kWHead);
+        if (head == kDeadHead || __ldcg(R + kWRc) != 0) continue;
+        if (atomicCAS(R + kWHead, head, kDeadHead) != head) continue;
+        uint32_t cur_slot = x, chead = head;
+        for (int hop = 0; hop < 64; ++hop) {
+            uint32_t* C = rec<W>(A, cur_slot);
+            uint32_t car = G.arity[chead & kSymMask];
+            uint32_t next = 0, nhead = 0;
+            for (uint32_t j = 0; j < car; ++j) {
+                uint32_t c = __ldcg(C + kWArgs + j);
+                if (atomicSub(rec<W>(A, c) + kWRc, 1u) == 1u && next == 0) {
+                    uint32_t h = __ldcg(rec<W>(A, c) + kWHead);
+                    if (h != kDeadHead && atomicCAS(rec<W>(A, c) + kWHead, h, kDeadHead) == h) {
+                        next = c;
+                        nhead = h;
+                    }
+                }
+            }
+            if (!next) break;
+            cur_slot = next;
+            chead = nhead;
+        }
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    // phase 2: live count per CTA range
+    const uint32_t span = bump - 1;
+    const uint32_t chunk = (span + nblocks - 1) / nblocks;
+    const uint32_t lo = 1 + block_rank * chunk;
+    const uint32_t hi = min(bump, lo + chunk);
+    uint32_t cnt = 0;
+    for (uint32_t x = lo + threadIdx.x; x < hi; x += kBlock) cnt += __ldcg(rec<W>(A, x) + kWHead) != kDeadHead;
+    uint32_t tot;
+    block_scan(cnt, &tot, sm);
+    if (threadIdx.x == 0) P.blocksum[block_rank] = tot;
+    grid_sync(P.ctl, nblocks, epoch);
+    // phase 3: prefix over CTA sums, then order-preserving scatter into the
+    // twin arena with the old -> new map
+    uint32_t prefix = 0, all = 0;
+    for (uint32_t b = threadIdx.x; b < nblocks; b += kBlock) {
+        uint32_t v = __ldcg(P.blocksum + b);
+        all += v;
+        if (b < block_rank) prefix += v;
+    }
+    {
+        uint32_t t1, t2;
+        block_scan(prefix, &t1, sm);
+        block_scan(all, &t2, sm);
+        prefix = t1;
+        all = t2;
+    }
+    uint32_t running = 1 + prefix;
+    for (uint32_t x0 = lo; x0 < hi; x0 += kBlock) {
+        uint32_t x = x0 + threadIdx.x;
+        bool live = x < hi && __ldcg(rec<W>(A, x) + kWHead) != kDeadHead;
+        uint32_t t;
+        uint32_t e = block_scan(live ? 1u : 0u, &t, sm);
+        if (x < hi) P.gcmap[x] = live ? running + e : 0u;
+        if (live) {
+            const uint4* src = reinterpret_cast<const uint4*>(rec<W>(A, x));
+            uint4* dst = reinterpret_cast<uint4*>(rec<W>(B, running + e));
+#pragma unroll
+            for (int q = 0; q < W / 4; ++q) dst[q] = __ldcg(src + q);
+        }
+        running += t;
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    // phase 4: remap args and waiters, and the frontier into one dense
+    // region of the other list buffer, and the roots
+    const uint32_t nbump = 1 + all;
+    for (uint32_t y = 1 + tid; y < nbump; y += nthreads) {
+        uint32_t* R = rec<W>(B, y);
+        uint32_t car = G.arity[R[kWHead] & kSymMask];
+        for (uint32_t j = 0; j < car; ++j) R[kWArgs + j] = __ldcg(P.gcmap + R[kWArgs + j]);
+        uint32_t w = R[kWWaiter];
+        if (w != 0 && w != kWoken) R[kWWaiter] = __ldcg(P.gcmap + w);
+    }
+    const uint32_t* Lin = P.list[cur];
+    uint32_t* Lout = P.list[cur ^ 1];
+    for (uint32_t v = tid; v < in.M; v += nthreads) Lout[v] = __ldcg(P.gcmap + Lin[frontier_phys(in, v)]);
+    for (uint32_t e = tid; e < P.num_roots; e += nthreads) P.roots[e] = __ldcg(P.gcmap + P.roots[e]);
+    if (block_rank == 0 && threadIdx.x == 0) {
+        region_off(P, cur ^ 1)[0] = 0;
+        region_cnt(P, cur ^ 1)[0] = in.M;
+        P.ctl->nregions[cur ^ 1] = 1;
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    arena_idx ^= 1;
+    return nbump;
+}
+
+}  // namespace trs_b200

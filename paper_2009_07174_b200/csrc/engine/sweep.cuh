@@ -1,0 +1,733 @@
+// The step loop: one persistent cooperative launch runs every sweep.
+//
+// A sweep (the reference's derive_phase + fold, sweep_engine.cpp:69-188)
+// processes the awake frontier in 32-entry chunks, one entry per lane, with
+// warps running independently: no CTA-wide barrier inside a sweep.
+//  * Fresh slots come from per-warp slabs (one atomic per slab, not per
+//    rewrite; get_new_index, term_store.cpp:118-138).
+//  * Next-frontier pushes go to the CTA's own region of the output list,
+//    sized in closed form (cta_prefix), through a shared-memory counter; the
+//    region table (offset, count, rewrites) is read back after the grid
+//    barrier, so a sweep has no contended global atomics at all.
+//  * Tiny frontiers run on CTA 0 alone out of shared memory (single-CTA
+//    mode), and frontiers of <= 32 slots on one warp of it (warp mode),
+//    with __syncthreads / __syncwarp instead of the grid barrier.
+#pragma once
+
+#include "gc.cuh"
+
+namespace trs_b200 {
+
+enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild };
+
+struct Slab {
+    uint32_t cur, end;  // warp-uniform: [cur, end) are this warp's unused fresh slots
+};
+
+// Mark a warp's unused slab slots dead so collections and copies skip them.
+template <int W>
+__device__ __forceinline__ void abandon_slab(uint32_t* arena, Slab& slab) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t x = slab.cur + lane; x < slab.end; x += 32) rec<W>(arena, x)[kWHead] = kDeadHead;
+    slab.cur = slab.end = 0;
+}
+
+struct StepCtx {
+    uint32_t s;           // sweep number (nf epoch of this sweep)
+    uint32_t bump;        // slot base of claims made during this sweep
+    uint32_t* claim_ctr;  // slots claimed during this sweep (relative to bump)
+    uint32_t* out;        // output region of the next frontier
+    uint32_t* push_ctr;   // entries pushed into `out` (shared memory)
+    uint32_t* abort_flag; // shared flag raised with ctl->abort_capacity (may be null)
+};
+
+struct PhaseClock {
+    long long t[4] = {0, 0, 0, 0};  // match, claim, apply, push (debug accounting)
+};
+
+// One entry per lane: derive (sweep_engine.cpp:163-188), claim, apply
+// (:190-258), push.  Every lane of the warp must call it (valid or not).
+// Returns the warp's number of rewrites.
+template <int W>
+__device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
+                                              Slab& slab, bool valid, uint32_t i, bool prof, PhaseClock& pc) {
+    constexpr int MAXA = W - 4;
+    const uint32_t s = C.s;
+    const uint32_t lane = threadIdx.x & 31;
+    long long c0 = prof ? clock64() : 0;
+    uint32_t act = kActNone;
+    uint32_t sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
+    uint32_t a[MAXA];
+    uint32_t bind[kMaxVars];
+    if (valid) {
+        uint32_t* R = rec<W>(arena, i);
+        uint2 he = *reinterpret_cast<const uint2*>(R);
+        sym = he.x & kSymMask;
+        cursor = he.x >> kSymBits;
+        ar = G.arity[sym];
+        load_args<W>(R, ar, a);
+        // subterm scan (sweep_engine.cpp:173-178); all child probes issue together
+        uint32_t ch[MAXA];
+        uint32_t cep[MAXA];
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j) {
+            ch[j] = 0;
+            cep[j] = 1;
+            if ((uint32_t)j < ar) {
+                uint2 c = *reinterpret_cast<const uint2*>(rec<W>(arena, a[j]));
+                ch[j] = c.x & kSymMask;
+                cep[j] = c.y;
+            }
+        }
+        bool pending = false;
+#pragma unroll
+        for (int j = MAXA - 1; j >= 0; --j) {
+            // nf_read(c) at sweep s: nf since an earlier sweep (sweep_engine.cpp:80-81)
+            if ((uint32_t)j >= cursor && (uint32_t)j < ar && (cep[j] == 0 || cep[j] >= s)) {
+                pending = true;
+                wpos = j;
+            }
+        }
+        if (pending) {
+            act = kActWait;
+            wchild = pick(a, wpos);
+        } else {
+            // first matching rule in source order (dispatch.hpp:119-130)
+            uint32_t stepnode[kMaxRuleSteps];
+            int chosen = -1;
+            for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
+                const DRule& Rl = G.rules[r];
+                bool ok = true;
+                for (uint32_t t = 0; t < Rl.num_steps; ++t) {
+                    const DStep st = G.steps[Rl.first_step + t];
+                    uint32_t node, head;
+                    if (st.parent < 0) {
+                        node = pick(a, st.child);
+                        head = pick(ch, st.child);
+                    } else {
+                        node = rec<W>(arena, stepnode[st.parent])[kWArgs + st.child];
+                        head = st.kind == 0 ? (rec<W>(arena, node)[kWHead] & kSymMask) : 0;
+                    }
+                    stepnode[t] = node;
+                    if (st.kind == 0) {
+                        if (head != st.value) {
+                            ok = false;
+                            break;
+                        }
+                    } else {
+                        bind[st.value] = node;
+                    }
+                }
+                if (ok) {
+                    chosen = (int)r;
+                    break;
+                }
+            }
+            if (chosen < 0) {
+                act = kActNf;
+            } else {
+                rule = (uint32_t)chosen;
+                act = G.rules[rule].collapse ? kActCollapse : kActBuild;
+            }
+        }
+    }
+    long long c1 = prof ? clock64() : 0;
+    if (prof) pc.t[0] += c1 - c0;
+
+    // ---- claim fresh slots from the warp's slab
+    const uint32_t need = act == kActBuild ? G.rules[rule].new_slots : 0;
+    const uint32_t incl = warp_incl_scan(need);
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    uint32_t fresh = 0;
+    if (total) {
+        if (slab.end - slab.cur < total) {
+            abandon_slab<W>(arena, slab);
+            uint32_t size = max(P.slab, total);
+            uint32_t off = 0;
+            if (lane == 0) {
+                off = atomicAdd(C.claim_ctr, size);
+                if ((uint64_t)C.bump + off + size > P.capacity && P.fixed_capacity) {
+                    // a full slab does not fit: take exactly what this step needs
+                    size = total;
+                    off = atomicAdd(C.claim_ctr, size);
+                }
+            }
+            off = __shfl_sync(0xffffffffu, off, 0);
+            size = __shfl_sync(0xffffffffu, size, 0);
+            const uint64_t start = (uint64_t)C.bump + off;
+            if (start + size > P.capacity) {
+                // fixed capacity exhausted: the reference raises Capacity (sweep_engine.cpp:221-226)
+                if (lane == 0) {
+                    atomicExch(&P.ctl->abort_capacity, 1u);
+                    if (C.abort_flag) *C.abort_flag = 1u;
+                }
+                if (act == kActBuild) act = kActNone;
+            } else {
+                slab.cur = (uint32_t)start;
+                slab.end = (uint32_t)(start + size);
+            }
+        }
+        if (slab.end - slab.cur >= total) {
+            fresh = slab.cur + incl - need;
+            slab.cur += total;
+        }
+    }
+    long long c2 = prof ? clock64() : 0;
+    if (prof) pc.t[1] += c2 - c1;
+
+    // ---- apply
+    uint32_t npush = 0, push1 = 0, push_mask = 0;
+    bool rewrote = false;
+    if (act == kActWait) {
+        if (wpos != cursor) rec<W>(arena, i)[kWHead] = sym | (wpos << kSymBits);
+        // subscribe to the pending child; a lost race (another subscriber,
+        // or the child turned nf this very sweep) means polling next sweep
+        uint32_t old = atomicCAS(rec<W>(arena, wchild) + kWWaiter, 0u, i);
+        if (old != 0) {
+            npush = 1;
+            push1 = i;
+        }
+    } else if (act == kActNf) {
+        uint32_t* R = rec<W>(arena, i);
+        R[kWEpoch] = s;
+        uint32_t w = atomicExch(R + kWWaiter, kWoken);
+        if (w != 0 && w != kWoken) {
+            npush = 1;
+            push1 = w;
+        }
+    } else if (act == kActCollapse) {
+        const DRule& Rl = G.rules[rule];
+        uint32_t src = bind[Rl.root_ref];
+        uint32_t* S = rec<W>(arena, src);
+        uint32_t shead = S[kWHead] & kSymMask;
+        uint32_t sar = G.arity[shead];
+        uint32_t b[MAXA];
+        load_args<W>(S, sar, b);
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j)
+            if ((uint32_t)j >= sar) b[j] = 0;
+        uint32_t* R = rec<W>(arena, i);
+        *reinterpret_cast<uint2*>(R) = make_uint2(shead, s);
+        store_args<W>(R, b, ar > sar ? ar : sar);
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j)
+            if ((uint32_t)j < sar) atomicAdd(rec<W>(arena, b[j]) + kWRc, 1u);
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j)
+            if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
+        uint32_t w = atomicExch(R + kWWaiter, kWoken);
+        if (w != 0 && w != kWoken) {
+            npush = 1;
+            push1 = w;
+        }
+        rewrote = true;
+    } else if (act == kActBuild) {
+        const DRule& Rl = G.rules[rule];
+        const uint32_t nfresh = Rl.new_slots;
+        for (uint32_t k = 0; k <= nfresh; ++k) {
+            const DInstr I = G.instrs[Rl.first_instr + k];
+            const uint32_t iar = G.arity[I.symbol];
+            uint32_t b[MAXA];
+#pragma unroll
+            for (int j = 0; j < MAXA; ++j) {
+                b[j] = 0;
+                if ((uint32_t)j < iar) {
+                    uint16_t ref = G.refs[I.first_ref + j];
+                    b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : bind[ref];
+                }
+            }
+            if (k < nfresh) {
+                uint32_t sub = I.subscriber == kNone ? 0u : I.subscriber == kRootSub ? i : fresh + I.subscriber;
+                uint32_t* F = rec<W>(arena, fresh + k);
+                *reinterpret_cast<uint4*>(F) = make_uint4(I.symbol | ((uint32_t)I.cursor << kSymBits), 0u, I.indegree, sub);
+#pragma unroll
+                for (int q = 0; q < MAXA / 4; ++q)
+                    *reinterpret_cast<uint4*>(F + kWArgs + q * 4) =
+                        make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
+            } else {
+                uint32_t* R = rec<W>(arena, i);
+                R[kWHead] = I.symbol | ((uint32_t)Rl.root_cursor << kSymBits);
+                store_args<W>(R, b, ar > iar ? ar : iar);
+            }
+            // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
+#pragma unroll
+            for (int j = 0; j < MAXA; ++j) {
+                if ((uint32_t)j < iar) {
+                    uint16_t ref = G.refs[I.first_ref + j];
+                    if (!(ref & kRefNode)) atomicAdd(rec<W>(arena, b[j]) + kWRc, 1u);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j)
+            if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
+        push_mask = Rl.push_mask;
+        npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
+        push1 = i;
+        rewrote = true;
+    }
+    long long c3 = prof ? clock64() : 0;
+    if (prof) pc.t[2] += c3 - c2;
+
+    // ---- next frontier: one shared-memory reservation per warp step
+    const uint32_t pincl = warp_incl_scan(npush);
+    const uint32_t ptotal = __shfl_sync(0xffffffffu, pincl, 31);
+    if (ptotal) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(C.push_ctr, ptotal);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        uint32_t pos = base + pincl - npush;
+        if (npush) {
+            if (act == kActBuild) {
+                uint32_t mask = push_mask;
+                while (mask) {
+                    uint32_t k = __ffs(mask) - 1;
+                    mask &= mask - 1;
+                    C.out[pos++] = fresh + k;
+                }
+                if (G.rules[rule].root_wait == kNone) C.out[pos++] = i;
+            } else {
+                C.out[pos] = push1;
+            }
+        }
+    }
+    if (prof) pc.t[3] += clock64() - c3;
+    return __popc(__ballot_sync(0xffffffffu, rewrote));
+}
+
+// All warps of CTAs [block_rank, nblocks) process the frontier in 32-entry
+// chunks; returns this thread's share of the rewrite count (lane 0 of each
+// warp holds its warp's count).
+template <int W>
+__device__ __forceinline__ unsigned long long cta_entries(const Params& P, const Prog& G, uint32_t* arena,
+                                                          const StepCtx& C, const Frontier& F,
+                                                          const uint32_t* __restrict__ in, uint32_t block_rank,
+                                                          uint32_t nblocks, Slab& slab, bool prof, PhaseClock& pc) {
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t gw = nblocks * kWarps;
+    unsigned long long rw = 0;
+    for (uint32_t k = block_rank * kWarps + warp; k * 32 < F.M; k += gw) {
+        const uint32_t v = k * 32 + lane;
+        const bool valid = v < F.M;
+        const uint32_t i = valid ? in[frontier_phys(F, v)] : 0u;
+        rw += warp_step<W>(P, G, arena, C, slab, valid, i, prof && warp == 0, pc);
+    }
+    return lane == 0 ? rw : 0ull;
+}
+
+// ---------------------------------------------------------------------------
+
+struct Local {
+    uint32_t sweep, cur, arena, bump;
+    unsigned long long total, maxw;
+    uint32_t gc_runs, small_sweeps, last_gc, peak_bump;
+    unsigned long long gc_ns;
+};
+
+__device__ __forceinline__ void load_local(Local& L, Ctl* c) {
+    L.sweep = __ldcg(&c->sweep);
+    L.cur = __ldcg(&c->cur);
+    L.arena = __ldcg(&c->arena);
+    L.bump = __ldcg(&c->bump);
+    L.total = __ldcg(&c->total_rewrites);
+    L.maxw = __ldcg(&c->max_width);
+    L.gc_runs = __ldcg(&c->gc_runs);
+    L.small_sweeps = __ldcg(&c->small_sweeps);
+    L.last_gc = __ldcg(&c->last_gc_sweep);
+    L.peak_bump = __ldcg(&c->peak_bump);
+    L.gc_ns = __ldcg(&c->gc_ns);
+}
+
+__device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
+    c->sweep = L.sweep;
+    c->cur = L.cur;
+    c->arena = L.arena;
+    c->bump = L.bump;
+    c->total_rewrites = L.total;
+    c->max_width = L.maxw;
+    c->gc_runs = L.gc_runs;
+    c->small_sweeps = L.small_sweeps;
+    c->last_gc_sweep = L.last_gc;
+    c->peak_bump = L.peak_bump;
+    c->gc_ns = L.gc_ns;
+    __threadfence();
+}
+
+// What to do before sweep s; identical in every CTA (pure function of Local).
+enum Plan : uint32_t { kPlanSweep, kPlanGc, kPlanGrow, kPlanFinish, kPlanTrace };
+
+__device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32_t m, bool just_collected,
+                                         uint32_t nwarps) {
+    const uint32_t s = L.sweep + 1;
+    if (s - P.sweep0 > P.trace_cap) return kPlanTrace;
+    if (m == 0) return kPlanFinish;
+    // worst case: every frontier slot rewrites with the largest template,
+    // plus what slab hand-offs can strand (ensure_headroom, sweep_engine.cpp:290-303)
+    const uint64_t need = (uint64_t)m * P.max_new;
+    const uint64_t worst = (uint64_t)L.bump + 2 * need + (uint64_t)nwarps * P.slab + 1;
+    const uint64_t tight = (uint64_t)L.bump + need + 1;
+    if ((P.fixed_capacity ? tight : worst) > P.capacity) {
+        if (P.allow_gc && !just_collected && !P.prefer_grow) return kPlanGc;
+        if (!P.fixed_capacity) return kPlanGrow;
+        // fixed capacity: go ahead; a claim that does not fit aborts with
+        // Capacity like the reference (sweep_engine.cpp:221-226)
+    }
+    // a collection that left the arena more than half full: grow instead of
+    // collecting again next sweep
+    if (just_collected && !P.fixed_capacity && (uint64_t)L.bump * 2 > P.capacity) return kPlanGrow;
+    if (P.allow_gc && P.gc_interval && !just_collected && s - L.last_gc >= P.gc_interval) return kPlanGc;
+    return kPlanSweep;
+}
+
+__device__ __forceinline__ void record(const Params& P, uint32_t s, unsigned long long width, const Local& L,
+                                       uint32_t m, uint32_t mode, uint64_t ns) {
+    const uint32_t k = s - P.sweep0;
+    if (k == 0 || k > P.trace_cap) return;
+    trs_gpu_sweep_record r;
+    r.sweep = k;
+    r.live_terms = L.bump - 1;  // allocated and not yet reclaimed by a compaction
+    r.rewrites = width;
+    r.n = L.bump;
+    r.free_len = 0;
+    r.active = m;
+    r.mode = mode;
+    r.micros_x1000 = ns;
+    P.trace[k - 1] = r;
+}
+
+// Shared-memory staging of a frontier's region table: prefix over counts,
+// offsets, and the sum of the per-region rewrite counts (the width of the
+// sweep that wrote the buffer).  Ends synchronised.
+__device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t* f_pref, uint32_t* f_off, Smem& sm,
+                                   unsigned long long* width) {
+    const uint32_t R = __ldcg(&P.ctl->nregions[buf]);
+    const uint32_t t0 = threadIdx.x, t1 = threadIdx.x + kBlock;
+    uint32_t c0 = t0 < R ? __ldcg(region_cnt(P, buf) + t0) : 0u;
+    uint32_t c1 = t1 < R ? __ldcg(region_cnt(P, buf) + t1) : 0u;
+    if (t0 < R) f_off[t0] = __ldcg(region_off(P, buf) + t0);
+    if (t1 < R) f_off[t1] = __ldcg(region_off(P, buf) + t1);
+    unsigned long long rw = 0;
+    if (width) {
+        if (t0 < R) rw += __ldcg(P.region_rew + buf * kMaxGrid + t0);
+        if (t1 < R) rw += __ldcg(P.region_rew + buf * kMaxGrid + t1);
+    }
+    uint32_t tot;
+    const uint32_t e0 = block_scan(c0, &tot, sm);
+    const uint32_t tot0 = tot;
+    const uint32_t e1 = block_scan(c1, &tot, sm);
+    if (t0 < R) f_pref[t0] = e0;
+    if (t1 < R) f_pref[t1] = tot0 + e1;
+    if (threadIdx.x == 0) f_pref[R] = tot0 + tot;
+    if (width) *width = block_sum64(rw, sm);  // synchronises
+    __syncthreads();
+    Frontier F;
+    F.R = R;
+    F.M = tot0 + tot;
+    F.pref = f_pref;
+    F.off = f_off;
+    return F;
+}
+
+// Shared-memory state of the single-CTA mode.
+struct SmallState {
+    uint32_t count[2];  // frontier counts: [sc] being read, [sc ^ 1] being pushed
+    uint32_t claim;     // slots claimed during the current sweep
+    uint32_t abort;     // a claim did not fit the fixed capacity
+    uint32_t sc;
+    uint32_t pad[3];
+    Local L;            // hand-over from warp mode to the whole CTA
+};
+
+// Warp 0 of CTA 0 runs sweeps alone while the frontier fits one warp.
+template <int W>
+__device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, SmallState& ss, Local& L,
+                            bool& just_collected, Slab& slab) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t* arena = P.arena[L.arena];
+    PhaseClock pc;
+    const bool prof = P.profile && lane == 0;
+    for (;;) {
+        const uint32_t sc = ss.sc;
+        const uint32_t m = ss.count[sc];
+        if (m == 0 || m > 32) break;
+        if (plan(P, L, m, just_collected, 1) != kPlanSweep) break;
+        just_collected = false;
+        const uint32_t s = L.sweep + 1;
+        const uint64_t t0 = global_ns();
+        const long long cs = prof ? clock64() : 0;
+        if (lane == 0) {
+            ss.count[sc ^ 1] = 0;
+            ss.claim = 0;
+        }
+        __syncwarp();
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
+        const bool valid = lane < m;
+        const uint32_t i = valid ? slist[sc * kSmallCap + lane] : 0u;
+        const uint32_t width = warp_step<W>(P, G, arena, C, slab, valid, i, prof, pc);
+        __syncwarp();
+        L.bump += ss.claim;
+        L.peak_bump = max(L.peak_bump, L.bump);
+        L.total += width;
+        L.maxw = width > L.maxw ? width : L.maxw;
+        L.sweep = s;
+        L.small_sweeps++;
+        if (lane == 0) {
+            ss.sc = sc ^ 1;
+            record(P, s, width, L, m, 2, global_ns() - t0);
+            if (P.profile) {
+                for (int k = 0; k < 4; ++k) P.ctl->prof[k] += pc.t[k];
+                P.ctl->prof[4] += clock64() - cs;
+                P.ctl->prof[5] += 1;
+                pc = PhaseClock{};
+            }
+        }
+        __syncwarp();
+        if (L.total > P.step_budget || ss.abort) break;
+    }
+}
+
+// CTA 0 runs sweeps out of shared memory while the frontier is small.
+template <int W>
+__device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bool& just_collected,
+                          uint32_t* slist, SmallState& ss, const Frontier& F, Slab& slab) {
+    Ctl* ctl = P.ctl;
+    const uint32_t cap_m = kSmallCap / (P.max_new + 1);
+    const uint32_t exit_m = min(P.small_exit, cap_m);
+    if (F.M > exit_m) {
+        // too wide for the shared-memory lists; nothing touched
+        if (threadIdx.x == 0) store_local(L, ctl);
+        return;
+    }
+    const uint32_t* gin = P.list[L.cur];
+    for (uint32_t v = threadIdx.x; v < F.M; v += kBlock) slist[v] = gin[frontier_phys(F, v)];
+    if (threadIdx.x == 0) {
+        ss.count[0] = F.M;
+        ss.sc = 0;
+        ss.abort = 0;
+    }
+    __syncthreads();
+    uint32_t* arena = P.arena[L.arena];
+    const uint32_t warp = threadIdx.x >> 5;
+    for (;;) {
+        const uint32_t sc = ss.sc;
+        const uint32_t m = ss.count[sc];
+        if (m > exit_m) break;
+        if (plan(P, L, m, just_collected, kWarps) != kPlanSweep) break;
+        if (P.warp_mode && m <= 32) {
+            if (warp == 0) {
+                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab);
+                if ((threadIdx.x & 31) == 0) ss.L = L;
+            }
+            __syncthreads();
+            L = ss.L;
+            just_collected = false;
+            if (L.total > P.step_budget || ss.abort) break;
+            if (ss.count[ss.sc] <= 32) break;  // warp mode stopped for another reason (plan / empty)
+            continue;
+        }
+        just_collected = false;
+        const uint32_t s = L.sweep + 1;
+        const uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
+        const long long cs = (P.profile && threadIdx.x == 0) ? clock64() : 0;
+        __syncthreads();  // everyone has read ss.count[sc]
+        if (threadIdx.x == 0) {
+            ss.count[sc ^ 1] = 0;
+            ss.claim = 0;
+        }
+        __syncthreads();
+        Frontier Fs{1, m, nullptr, nullptr};
+        uint32_t zero_off = 0;
+        Fs.off = &zero_off;
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
+        PhaseClock pc;
+        unsigned long long rw = cta_entries<W>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
+                                               P.profile && threadIdx.x == 0, pc);
+        const unsigned long long width = block_sum64(rw, sm);
+        L.bump += ss.claim;
+        L.peak_bump = max(L.peak_bump, L.bump);
+        L.total += width;
+        L.maxw = width > L.maxw ? width : L.maxw;
+        L.sweep = s;
+        L.small_sweeps++;
+        if (threadIdx.x == 0) {
+            ss.sc = sc ^ 1;
+            record(P, s, width, L, m, 1, global_ns() - t0);
+            if (P.profile) {
+                for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
+                ctl->prof[4] += clock64() - cs;
+                ctl->prof[5] += 1;
+            }
+        }
+        __syncthreads();
+        if (L.total > P.step_budget || ss.abort) break;
+    }
+    // hand the frontier back to the grid as one region of the global list
+    const uint32_t m = ss.count[ss.sc];
+    uint32_t* gout = P.list[L.cur];
+    for (uint32_t v = threadIdx.x; v < m; v += kBlock) gout[v] = slist[ss.sc * kSmallCap + v];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        region_off(P, L.cur)[0] = 0;
+        region_cnt(P, L.cur)[0] = m;
+        ctl->nregions[L.cur] = 1;
+        store_local(L, ctl);
+    }
+}
+
+template <int W, int MINB>
+__global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
+    extern __shared__ __align__(16) uint8_t smem_raw[];
+    __shared__ Smem sm;
+    __shared__ SmallState ss;
+    __shared__ uint32_t f_pref[kMaxGrid + 1];
+    __shared__ uint32_t f_off[kMaxGrid];
+    __shared__ uint32_t s_push;
+    // stage the program tables; the single-CTA frontier lists follow them
+    for (uint32_t o = threadIdx.x * 16; o < P.prog_bytes; o += kBlock * 16)
+        *reinterpret_cast<uint4*>(smem_raw + o) = *reinterpret_cast<const uint4*>(P.prog + o);
+    __syncthreads();
+    const Prog G = view_prog(smem_raw);
+    uint32_t* slist = reinterpret_cast<uint32_t*>(smem_raw + P.prog_bytes);
+    const uint32_t nblocks = gridDim.x;
+    const uint32_t nwarps = nblocks * kWarps;
+    const bool leader = blockIdx.x == 0 && threadIdx.x == 0;
+    Ctl* ctl = P.ctl;
+
+    Local L;
+    load_local(L, ctl);
+    bool just_collected = false;
+    uint32_t exit_status = kRunning;
+    uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
+    Slab slab{0, 0};
+    Frontier F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+
+    auto collect = [&]() {
+        abandon_slab<W>(P.arena[L.arena], slab);
+        grid_sync(ctl, nblocks, epoch);  // every slab is marked before the collector scans
+        const uint64_t t0 = global_ns();
+        L.bump = gc_compact<W>(P, sm, G, L.arena, L.bump, F, L.cur, blockIdx.x, nblocks, epoch);
+        L.cur ^= 1;
+        L.gc_runs++;
+        L.gc_ns += global_ns() - t0;
+        F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+    };
+
+    if (P.compact_only) {
+        // final compaction: collect until a pass reclaims nothing
+        for (uint32_t round = 0; round < P.compact_only; ++round) {
+            const uint32_t before = L.bump;
+            collect();
+            if (L.bump == before) break;
+        }
+        if (leader) {
+            store_local(L, ctl);
+            ctl->status = kDone;
+        }
+        return;
+    }
+
+    for (;;) {
+        const uint32_t s = L.sweep + 1;
+        const uint32_t m = F.M;
+        const uint32_t pl = plan(P, L, m, just_collected, nwarps);
+        if (pl == kPlanFinish) {
+            // the first sweep whose frontier is empty (sweep_engine.cpp:147)
+            if (leader) record(P, s, 0, L, 0, 0, 0);
+            L.sweep = s;
+            exit_status = kDone;
+            break;
+        }
+        if (pl == kPlanTrace) {
+            exit_status = kNeedTrace;
+            break;
+        }
+        if (pl == kPlanGrow) {
+            exit_status = kNeedGrow;
+            break;
+        }
+        if (pl == kPlanGc) {
+            collect();
+            L.last_gc = L.sweep + 1;
+            just_collected = true;
+            continue;
+        }
+
+        if (m <= P.small_enter) {
+            // ---- single-CTA mode: CTA 0 runs sweeps out of shared memory,
+            // the rest of the grid parks in the barrier
+            const uint32_t before = L.sweep;
+            if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss, F, slab);
+            grid_sync(ctl, nblocks, epoch, /*park=*/blockIdx.x != 0);
+            load_local(L, ctl);
+            F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+            if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
+            if (__ldcg(&ctl->abort_capacity)) {
+                exit_status = kCapacity;
+                break;
+            }
+            if (L.total > P.step_budget) {
+                exit_status = kStepBudget;
+                break;
+            }
+            if (L.sweep != before) continue;
+            // no progress in single-CTA mode (frontier too wide for its
+            // lists): fall through to one grid-wide sweep
+        }
+        just_collected = false;
+
+        // ---- grid-wide sweep
+        const uint64_t t0 = leader ? global_ns() : 0;
+        const long long cs = (P.profile && leader) ? clock64() : 0;
+        if (threadIdx.x == 0) s_push = 0;
+        __syncthreads();
+        const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks);
+        uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
+        if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
+        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + out_off, &s_push, nullptr};
+        PhaseClock pc;
+        unsigned long long rw = cta_entries<W>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks,
+                                               slab, P.profile && leader, pc);
+        rw = block_sum64(rw, sm);
+        if (threadIdx.x == 0) {
+            region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
+            region_cnt(P, L.cur ^ 1)[blockIdx.x] = s_push;
+            P.region_rew[(L.cur ^ 1) * kMaxGrid + blockIdx.x] = rw;
+        }
+        if (leader) ctl->nregions[L.cur ^ 1] = nblocks;
+        grid_sync(ctl, nblocks, epoch);
+        L.cur ^= 1;
+        unsigned long long width = 0;
+        F = stage_frontier(P, L.cur, f_pref, f_off, sm, &width);
+        const uint32_t allocd = __ldcg(claim_ctr);
+        L.bump += allocd;
+        L.peak_bump = max(L.peak_bump, L.bump);
+        L.total += width;
+        L.maxw = width > L.maxw ? width : L.maxw;
+        L.sweep = s;
+        if (leader) {
+            record(P, s, width, L, m, 0, global_ns() - t0);
+            if (P.profile) {
+                for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
+                ctl->prof[4] += clock64() - cs;
+                ctl->prof[5] += 1;
+            }
+        }
+        if (__ldcg(&ctl->abort_capacity)) {
+            exit_status = kCapacity;
+            break;
+        }
+        if (L.total > P.step_budget) {
+            exit_status = kStepBudget;
+            break;
+        }
+    }
+    // leave no half-used slab behind: the host may copy or the next launch
+    // may collect [0, bump)
+    abandon_slab<W>(P.arena[L.arena], slab);
+    if (leader) {
+        store_local(L, ctl);
+        ctl->status = exit_status;
+    }
+}
+
+}  // namespace trs_b200
