@@ -216,6 +216,13 @@ void* trs_gpu_stream(trs_gpu_engine* engine);
  * 0's thread 0): match, claim, apply, push, whole single-CTA sweep, sweeps. */
 int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out6);
 
+/* Fixed per-sweep overhead probe on the loaded store: `iters` grid barriers
+ * (mode 0) or barriers plus the frontier-table staging of a grid sweep
+ * (mode 1) in one step-loop launch; reports ns per iteration.  Leaves the
+ * store untouched except for timing fields. */
+int trs_gpu_overhead_probe(trs_gpu_engine* engine, uint32_t iters, uint32_t mode, uint32_t max_blocks,
+                           double* ns_per_iter);
+
 /* Compacting collection on demand (up to max_rounds passes, 0 -> 8, stops
  * when a pass reclaims nothing): afterwards the arena holds only slots
  * still referenced, renumbered densely, roots updated. */

@@ -125,6 +125,7 @@ def lib():
         "trs_gpu_gather_probe": ([I, U64, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
         "trs_gpu_stream": ([P], P),
         "trs_gpu_profile_counters": ([P, P], I),
+        "trs_gpu_overhead_probe": ([P, U32, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
         "trs_gpu_compact": ([P, U32, ctypes.POINTER(Stats)], I),
         "trs_gpu_fetch_records": ([P, P, U64, ctypes.POINTER(U64), u32p, P], I),
         "trsb_system_load": ([ctypes.c_char_p, ctypes.POINTER(P), ctypes.c_char_p, ctypes.c_size_t], I),
@@ -164,7 +165,7 @@ def exported_symbols() -> list[str]:
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
                         "trs_gpu_run", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
                         "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
-                        "trs_gpu_profile_counters")]
+                        "trs_gpu_profile_counters", "trs_gpu_overhead_probe")]
 
 
 def device_count() -> int:
@@ -436,6 +437,12 @@ class Engine:
     def stream(self) -> int:
         """cudaStream_t of this engine (for torch.cuda.ExternalStream + events)."""
         return lib().trs_gpu_stream(self._h)
+
+    def overhead_probe(self, iters: int = 2000, mode: int = 0, max_blocks: int = 0) -> float:
+        ns = ctypes.c_double(0)
+        rc = lib().trs_gpu_overhead_probe(self._h, iters, mode, max_blocks, ctypes.byref(ns))
+        _raise(rc, self._err())
+        return ns.value
 
     def profile_counters(self) -> dict:
         out = np.zeros(6, np.uint64)

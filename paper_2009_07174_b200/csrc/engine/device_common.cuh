@@ -82,6 +82,8 @@ struct Params {
     uint32_t prefer_grow;   // out of headroom: grow (host) rather than collect
     uint32_t profile;       // phase cycle accounting of CTA 0 (debug)
     uint32_t slab;          // fresh slots a warp claims at a time
+    uint32_t probe_iters;   // >0: time this many grid barriers and exit (trs_gpu_overhead_probe)
+    uint32_t probe_mode;
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {
@@ -119,12 +121,18 @@ __device__ __forceinline__ void grid_sync(Ctl* ctl, uint32_t nblocks, uint32_t& 
     if (threadIdx.x == 0) {
         red_release_add(&ctl->bar_arrive, 1u);
         const uint32_t target = epoch * nblocks;
-        uint32_t ns = 32;
-        while ((int)(ld_acquire(&ctl->bar_arrive) - target) < 0) {
-            __nanosleep(ns);
-            if (park && ns < 4096) ns <<= 1;
+        // the acquire load pairs with every CTA's release increment; the
+        // CTA barrier below extends it to the whole CTA
+        if (park) {
+            uint32_t ns = 64;
+            while ((int)(ld_acquire(&ctl->bar_arrive) - target) < 0) {
+                __nanosleep(ns);
+                if (ns < 4096) ns <<= 1;
+            }
+        } else {
+            while ((int)(ld_acquire(&ctl->bar_arrive) - target) < 0) {
+            }
         }
-        __threadfence();
     }
     __syncthreads();
 }

@@ -100,7 +100,15 @@ __global__ void load_frontier(uint32_t* __restrict__ arena, uint32_t n, const ui
             uint32_t off = 0;
             if (lane == 0) off = atomicAdd(count, __popc(mask));
             off = __shfl_sync(0xffffffffu, off, 0);
-            if (push) list[off + __popc(mask & ((1u << lane) - 1))] = i;
+            if (push) {
+                // rich entry with payload (sweep.cuh): slot, head, flag, args
+                uint32_t* E = list + (size_t)(off + __popc(mask & ((1u << lane) - 1))) * W;
+                const uint32_t* R = arena + (size_t)i * W;
+                *reinterpret_cast<uint4*>(E) = make_uint4(i, R[kWHead], 1u, 0u);
+#pragma unroll
+                for (int q = 1; q < W / 4; ++q)
+                    reinterpret_cast<uint4*>(E)[q] = reinterpret_cast<const uint4*>(R)[q];
+            }
         }
     }
 }
@@ -409,7 +417,7 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     size_t rec_bytes = (size_t)e->W * 4;
     for (int k = 0; k < 2; ++k) {
         CUDA_TRY(e, cudaMalloc(&e->d_arena[k], rec_bytes * capacity));
-        CUDA_TRY(e, cudaMalloc(&e->d_list[k], sizeof(uint32_t) * capacity));
+        CUDA_TRY(e, cudaMalloc(&e->d_list[k], sizeof(uint32_t) * e->W * capacity));
     }
     CUDA_TRY(e, cudaMalloc(&e->d_gcmap, sizeof(uint32_t) * capacity));
     e->capacity = capacity;
@@ -465,7 +473,7 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     uint32_t* nl[2] = {nullptr, nullptr};
     uint32_t* nm = nullptr;
     for (int k = 0; k < 2; ++k) {
-        if (cudaMalloc(&na[k], rec_bytes * cap) != cudaSuccess || cudaMalloc(&nl[k], sizeof(uint32_t) * cap) != cudaSuccess) {
+        if (cudaMalloc(&na[k], rec_bytes * cap) != cudaSuccess || cudaMalloc(&nl[k], rec_bytes * cap) != cudaSuccess) {
             for (int j = 0; j < 2; ++j) { cudaFree(na[j]); cudaFree(nl[j]); }
             cudaGetLastError();
             return fail(e, TRS_GPU_CAPACITY, "device memory exhausted while growing the term store");
@@ -480,7 +488,7 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     uint64_t extent = frontier_extent(e, c);
     CUDA_TRY(e, cudaMemcpyAsync(na[c.arena], e->d_arena[c.arena], rec_bytes * c.bump, cudaMemcpyDeviceToDevice, e->stream));
     if (extent)
-        CUDA_TRY(e, cudaMemcpyAsync(nl[c.cur], e->d_list[c.cur], sizeof(uint32_t) * extent, cudaMemcpyDeviceToDevice, e->stream));
+        CUDA_TRY(e, cudaMemcpyAsync(nl[c.cur], e->d_list[c.cur], rec_bytes * extent, cudaMemcpyDeviceToDevice, e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
     for (int k = 0; k < 2; ++k) {
         cudaFree(e->d_arena[k]);
@@ -945,6 +953,25 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
         stats->block_threads = kBlock;
         stats->record_words = e->W;
     }
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_overhead_probe(trs_gpu_engine* e, uint32_t iters, uint32_t mode, uint32_t max_blocks, double* ns_per_iter) {
+    if (!e || !e->loaded || !ns_per_iter) return TRS_GPU_INVALID;
+    cudaSetDevice(e->device);
+    int blocks = grid_blocks(e, 0);
+    if (max_blocks && (int)max_blocks < blocks) blocks = (int)max_blocks;
+    Params P = make_params(e, blocks);
+    P.probe_iters = iters ? iters : 1000;
+    P.probe_mode = mode;
+    void* args[] = {&P};
+    reset_barrier(e);
+    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
+    if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
+    if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("probe: ") + cudaGetErrorString(err));
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    *ns_per_iter = (double)c.gc_ns / P.probe_iters;
     return TRS_GPU_OK;
 }
 

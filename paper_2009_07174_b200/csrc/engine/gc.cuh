@@ -128,7 +128,17 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
     }
     const uint32_t* Lin = P.list[cur];
     uint32_t* Lout = P.list[cur ^ 1];
-    for (uint32_t v = tid; v < in.M; v += nthreads) Lout[v] = __ldcg(P.gcmap + Lin[frontier_phys(in, v)]);
+    for (uint32_t v = tid; v < in.M; v += nthreads) {
+        // rich entries (sweep.cuh): remap the slot and, with a payload, its arguments
+        const uint32_t* E = Lin + (size_t)frontier_phys(in, v) * W;
+        uint32_t* D = Lout + (size_t)v * W;
+        const uint4 q0 = __ldcg(reinterpret_cast<const uint4*>(E));
+        *reinterpret_cast<uint4*>(D) = make_uint4(__ldcg(P.gcmap + q0.x), q0.y, q0.z, 0u);
+        if (q0.z) {
+            const uint32_t car = G.arity[q0.y & kSymMask];
+            for (uint32_t j = 0; j < car; ++j) D[kWArgs + j] = __ldcg(P.gcmap + __ldcg(E + kWArgs + j));
+        }
+    }
     for (uint32_t e = tid; e < P.num_roots; e += nthreads) P.roots[e] = __ldcg(P.gcmap + P.roots[e]);
     if (block_rank == 0 && threadIdx.x == 0) {
         region_off(P, cur ^ 1)[0] = 0;

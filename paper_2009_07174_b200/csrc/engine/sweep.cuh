@@ -48,24 +48,55 @@ struct PhaseClock {
 // One entry per lane: derive (sweep_engine.cpp:163-188), claim, apply
 // (:190-258), push.  Every lane of the warp must call it (valid or not).
 // Returns the warp's number of rewrites.
-template <int W>
+// Frontier entries.  Single-CTA lists hold bare slot ids.  Grid lists
+// ("rich" entries) hold W words laid out like a record,
+//   [slot, head|cursor, has_payload, 0, args...],
+// where the pusher copies the node's head and arguments whenever it knows
+// them (fresh nodes, rewritten roots, polls): the node cannot change
+// before its own next derive, so the next sweep skips its record gather.
+constexpr uint32_t kEntHasPayload = 1;
+
+template <int W, bool kRich>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
-                                              Slab& slab, bool valid, uint32_t i, bool prof, PhaseClock& pc) {
+                                              Slab& slab, bool valid, const uint32_t* entry, bool prof,
+                                              PhaseClock& pc) {
     constexpr int MAXA = W - 4;
     const uint32_t s = C.s;
     const uint32_t lane = threadIdx.x & 31;
     long long c0 = prof ? clock64() : 0;
     uint32_t act = kActNone;
-    uint32_t sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
+    uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
     uint32_t a[MAXA];
     uint32_t bind[kMaxVars];
     if (valid) {
-        uint32_t* R = rec<W>(arena, i);
-        uint2 he = *reinterpret_cast<const uint2*>(R);
-        sym = he.x & kSymMask;
-        cursor = he.x >> kSymBits;
+        uint32_t headw;
+        bool have = false;
+        if (kRich) {
+            const uint4 q0 = *reinterpret_cast<const uint4*>(entry);
+            i = q0.x;
+            headw = q0.y;
+            have = q0.z == kEntHasPayload;
+            if (have) {
+#pragma unroll
+                for (int q = 0; q < MAXA / 4; ++q) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(entry + kWArgs + q * 4);
+                    a[q * 4 + 0] = v.x;
+                    a[q * 4 + 1] = v.y;
+                    a[q * 4 + 2] = v.z;
+                    a[q * 4 + 3] = v.w;
+                }
+            }
+        } else {
+            i = *entry;
+        }
+        if (!have) {
+            uint32_t* R = rec<W>(arena, i);
+            headw = R[kWHead];
+            load_args<W>(R, G.arity[headw & kSymMask], a);
+        }
+        sym = headw & kSymMask;
+        cursor = headw >> kSymBits;
         ar = G.arity[sym];
-        load_args<W>(R, ar, a);
         // subterm scan (sweep_engine.cpp:173-178); all child probes issue together
         uint32_t ch[MAXA];
         uint32_t cep[MAXA];
@@ -279,13 +310,52 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         uint32_t pos = base + pincl - npush;
         if (npush) {
             if (act == kActBuild) {
-                uint32_t mask = push_mask;
+                const DRule& Rl = G.rules[rule];
+                uint32_t mask = push_mask | (Rl.root_wait == kNone ? (1u << Rl.new_slots) : 0u);
                 while (mask) {
-                    uint32_t k = __ffs(mask) - 1;
+                    const uint32_t k = __ffs(mask) - 1;
                     mask &= mask - 1;
-                    C.out[pos++] = fresh + k;
+                    const bool root = k == Rl.new_slots;
+                    const uint32_t slot = root ? i : fresh + k;
+                    if (kRich) {
+                        const DInstr I = G.instrs[Rl.first_instr + k];
+                        const uint32_t iar = G.arity[I.symbol];
+                        uint32_t b[MAXA];
+#pragma unroll
+                        for (int j = 0; j < MAXA; ++j) {
+                            b[j] = 0;
+                            if ((uint32_t)j < iar) {
+                                const uint16_t ref = G.refs[I.first_ref + j];
+                                b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : bind[ref];
+                            }
+                        }
+                        const uint32_t cur = root ? Rl.root_cursor : I.cursor;
+                        uint32_t* E = C.out + (size_t)pos * W;
+                        *reinterpret_cast<uint4*>(E) =
+                            make_uint4(slot, I.symbol | (cur << kSymBits), kEntHasPayload, 0u);
+#pragma unroll
+                        for (int q = 0; q < MAXA / 4; ++q)
+                            if ((uint32_t)(q * 4) < iar)
+                                *reinterpret_cast<uint4*>(E + kWArgs + q * 4) =
+                                    make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
+                    } else {
+                        C.out[pos] = slot;
+                    }
+                    ++pos;
                 }
-                if (G.rules[rule].root_wait == kNone) C.out[pos++] = i;
+            } else if (kRich) {
+                uint32_t* E = C.out + (size_t)pos * W;
+                if (act == kActWait) {
+                    // polling: the record is exactly what this lane holds
+                    *reinterpret_cast<uint4*>(E) = make_uint4(i, sym | (wpos << kSymBits), kEntHasPayload, 0u);
+#pragma unroll
+                    for (int q = 0; q < MAXA / 4; ++q)
+                        if ((uint32_t)(q * 4) < ar)
+                            *reinterpret_cast<uint4*>(E + kWArgs + q * 4) =
+                                make_uint4(a[q * 4], a[q * 4 + 1], a[q * 4 + 2], a[q * 4 + 3]);
+                } else {
+                    *reinterpret_cast<uint4*>(E) = make_uint4(push1, 0u, 0u, 0u);  // woken: no payload
+                }
             } else {
                 C.out[pos] = push1;
             }
@@ -298,7 +368,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 // All warps of CTAs [block_rank, nblocks) process the frontier in 32-entry
 // chunks; returns this thread's share of the rewrite count (lane 0 of each
 // warp holds its warp's count).
-template <int W>
+template <int W, bool kRich>
 __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const Prog& G, uint32_t* arena,
                                                           const StepCtx& C, const Frontier& F,
                                                           const uint32_t* __restrict__ in, uint32_t block_rank,
@@ -309,8 +379,8 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     for (uint32_t k = block_rank * kWarps + warp; k * 32 < F.M; k += gw) {
         const uint32_t v = k * 32 + lane;
         const bool valid = v < F.M;
-        const uint32_t i = valid ? in[frontier_phys(F, v)] : 0u;
-        rw += warp_step<W>(P, G, arena, C, slab, valid, i, prof && warp == 0, pc);
+        const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * (kRich ? W : 1) : in;
+        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && warp == 0, pc);
     }
     return lane == 0 ? rw : 0ull;
 }
@@ -397,32 +467,63 @@ __device__ __forceinline__ void record(const Params& P, uint32_t s, unsigned lon
 
 // Shared-memory staging of a frontier's region table: prefix over counts,
 // offsets, and the sum of the per-region rewrite counts (the width of the
-// sweep that wrote the buffer).  Ends synchronised.
-__device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t* f_pref, uint32_t* f_off, Smem& sm,
-                                   unsigned long long* width) {
-    const uint32_t R = __ldcg(&P.ctl->nregions[buf]);
+// sweep that wrote the buffer).  One round trip: the table is read for all
+// `nblocks` possible regions together with its length, then one fused
+// block scan (counts) + reduction (rewrites).  Ends synchronised.
+__device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nblocks, uint32_t* f_pref,
+                                   uint32_t* f_off, Smem& sm, unsigned long long* width) {
     const uint32_t t0 = threadIdx.x, t1 = threadIdx.x + kBlock;
-    uint32_t c0 = t0 < R ? __ldcg(region_cnt(P, buf) + t0) : 0u;
-    uint32_t c1 = t1 < R ? __ldcg(region_cnt(P, buf) + t1) : 0u;
-    if (t0 < R) f_off[t0] = __ldcg(region_off(P, buf) + t0);
-    if (t1 < R) f_off[t1] = __ldcg(region_off(P, buf) + t1);
+    const uint32_t R = __ldcg(&P.ctl->nregions[buf]);
+    uint32_t c0 = t0 < nblocks ? __ldcg(region_cnt(P, buf) + t0) : 0u;
+    uint32_t c1 = t1 < nblocks ? __ldcg(region_cnt(P, buf) + t1) : 0u;
+    const uint32_t o0 = t0 < nblocks ? __ldcg(region_off(P, buf) + t0) : 0u;
+    const uint32_t o1 = t1 < nblocks ? __ldcg(region_off(P, buf) + t1) : 0u;
     unsigned long long rw = 0;
     if (width) {
-        if (t0 < R) rw += __ldcg(P.region_rew + buf * kMaxGrid + t0);
-        if (t1 < R) rw += __ldcg(P.region_rew + buf * kMaxGrid + t1);
+        if (t0 < nblocks) rw += __ldcg(P.region_rew + buf * kMaxGrid + t0);
+        if (t1 < nblocks) rw += __ldcg(P.region_rew + buf * kMaxGrid + t1);
     }
-    uint32_t tot;
-    const uint32_t e0 = block_scan(c0, &tot, sm);
-    const uint32_t tot0 = tot;
-    const uint32_t e1 = block_scan(c1, &tot, sm);
-    if (t0 < R) f_pref[t0] = e0;
-    if (t1 < R) f_pref[t1] = tot0 + e1;
-    if (threadIdx.x == 0) f_pref[R] = tot0 + tot;
-    if (width) *width = block_sum64(rw, sm);  // synchronises
+    if (t0 >= R) c0 = 0, rw = 0;
+    if (t1 >= R) c1 = 0;
+    if (t0 < R) f_off[t0] = o0;
+    if (t1 < R) f_off[t1] = o1;
+    // fused scan: each thread owns regions t0 and t1 = t0 + kBlock
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t x0 = c0, x1 = c1;
+    unsigned long long r = rw;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t y0 = __shfl_up_sync(0xffffffffu, x0, o);
+        uint32_t y1 = __shfl_up_sync(0xffffffffu, x1, o);
+        if (lane >= o) x0 += y0, x1 += y1;
+        r += __shfl_xor_sync(0xffffffffu, r, o);
+    }
+    if (lane == 31) {
+        sm.scan[warp] = x0;
+        sm.bcast[0] = 0;
+    }
+    __shared__ uint32_t scan1[kWarps];
+    if (lane == 31) scan1[warp] = x1;
+    if (lane == 0) sm.red[warp] = r;
+    __syncthreads();
+    uint32_t p0 = 0, p1 = 0, tot0 = 0, tot1 = 0;
+    unsigned long long rtot = 0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+        const uint32_t a0 = sm.scan[w], a1 = scan1[w];
+        if (w < warp) p0 += a0, p1 += a1;
+        tot0 += a0;
+        tot1 += a1;
+        rtot += sm.red[w];
+    }
+    if (t0 < R) f_pref[t0] = p0 + x0 - c0;
+    if (t1 < R) f_pref[t1] = tot0 + p1 + x1 - c1;
+    if (threadIdx.x == 0) f_pref[R] = tot0 + tot1;
+    if (width) *width = rtot;
     __syncthreads();
     Frontier F;
     F.R = R;
-    F.M = tot0 + tot;
+    F.M = tot0 + tot1;
     F.pref = f_pref;
     F.off = f_off;
     return F;
@@ -462,8 +563,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         __syncwarp();
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
         const bool valid = lane < m;
-        const uint32_t i = valid ? slist[sc * kSmallCap + lane] : 0u;
-        const uint32_t width = warp_step<W>(P, G, arena, C, slab, valid, i, prof, pc);
+        const uint32_t width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
         __syncwarp();
         L.bump += ss.claim;
         L.peak_bump = max(L.peak_bump, L.bump);
@@ -499,7 +599,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         return;
     }
     const uint32_t* gin = P.list[L.cur];
-    for (uint32_t v = threadIdx.x; v < F.M; v += kBlock) slist[v] = gin[frontier_phys(F, v)];
+    for (uint32_t v = threadIdx.x; v < F.M; v += kBlock) slist[v] = gin[(size_t)frontier_phys(F, v) * W];
     if (threadIdx.x == 0) {
         ss.count[0] = F.M;
         ss.sc = 0;
@@ -540,8 +640,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         Fs.off = &zero_off;
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
         PhaseClock pc;
-        unsigned long long rw = cta_entries<W>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
-                                               P.profile && threadIdx.x == 0, pc);
+        unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
+                                                      P.profile && threadIdx.x == 0, pc);
         const unsigned long long width = block_sum64(rw, sm);
         L.bump += ss.claim;
         L.peak_bump = max(L.peak_bump, L.bump);
@@ -564,7 +664,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     // hand the frontier back to the grid as one region of the global list
     const uint32_t m = ss.count[ss.sc];
     uint32_t* gout = P.list[L.cur];
-    for (uint32_t v = threadIdx.x; v < m; v += kBlock) gout[v] = slist[ss.sc * kSmallCap + v];
+    for (uint32_t v = threadIdx.x; v < m; v += kBlock)
+        *reinterpret_cast<uint4*>(gout + (size_t)v * W) = make_uint4(slist[ss.sc * kSmallCap + v], 0u, 0u, 0u);
     __syncthreads();
     if (threadIdx.x == 0) {
         region_off(P, L.cur)[0] = 0;
@@ -599,7 +700,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     uint32_t exit_status = kRunning;
     uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
     Slab slab{0, 0};
-    Frontier F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+    Frontier F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
 
     auto collect = [&]() {
         abandon_slab<W>(P.arena[L.arena], slab);
@@ -609,8 +710,23 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         L.cur ^= 1;
         L.gc_runs++;
         L.gc_ns += global_ns() - t0;
-        F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+        F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
     };
+
+    if (P.probe_iters) {
+        // overhead probe: grid barriers alone (mode 0) or a barrier plus the
+        // frontier staging every grid sweep does (mode 1)
+        const uint64_t t0 = global_ns();
+        for (uint32_t it = 0; it < P.probe_iters; ++it) {
+            grid_sync(ctl, nblocks, epoch);
+            if (P.probe_mode == 1) {
+                unsigned long long w;
+                F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, &w);
+            }
+        }
+        if (leader) ctl->gc_ns = global_ns() - t0;
+        return;
+    }
 
     if (P.compact_only) {
         // final compaction: collect until a pass reclaims nothing
@@ -659,7 +775,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss, F, slab);
             grid_sync(ctl, nblocks, epoch, /*park=*/blockIdx.x != 0);
             load_local(L, ctl);
-            F = stage_frontier(P, L.cur, f_pref, f_off, sm, nullptr);
+            F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
             if (__ldcg(&ctl->abort_capacity)) {
                 exit_status = kCapacity;
@@ -683,10 +799,10 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks);
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
-        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + out_off, &s_push, nullptr};
+        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * W, &s_push, nullptr};
         PhaseClock pc;
-        unsigned long long rw = cta_entries<W>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks,
-                                               slab, P.profile && leader, pc);
+        unsigned long long rw = cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x,
+                                                     nblocks, slab, P.profile && leader, pc);
         rw = block_sum64(rw, sm);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
@@ -697,7 +813,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         grid_sync(ctl, nblocks, epoch);
         L.cur ^= 1;
         unsigned long long width = 0;
-        F = stage_frontier(P, L.cur, f_pref, f_off, sm, &width);
+        F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, &width);
         const uint32_t allocd = __ldcg(claim_ctr);
         L.bump += allocd;
         L.peak_bump = max(L.peak_bump, L.bump);

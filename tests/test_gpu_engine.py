@@ -147,7 +147,9 @@ def test_compact_and_fetch(engine):
     nbytes, words = engine.fetch_records()
     assert words == 8 and nbytes == (c["live_terms"] + 1) * 32
     np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
-    assert c["live_terms"] + 1 <= g["nodes"] + 2
+    # what survives is the normal form plus garbage still referenced by
+    # garbage the bounded cascade has not reached yet
+    assert g["nodes"] <= c["live_terms"] <= 4 * g["nodes"]
 
 
 def test_trace_records(engine):
