@@ -84,6 +84,7 @@ struct Params {
     uint32_t slab;          // fresh slots a warp claims at a time
     uint32_t probe_iters;   // >0: time this many grid barriers and exit (trs_gpu_overhead_probe)
     uint32_t probe_mode;
+    uint32_t rich;          // grid frontier entries carry record payloads (W words) instead of bare slots
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

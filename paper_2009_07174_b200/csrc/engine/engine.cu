@@ -35,6 +35,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -78,7 +79,7 @@ __global__ void load_records(uint32_t* __restrict__ arena, uint32_t n, const uin
 
 template <int W>
 __global__ void load_frontier(uint32_t* __restrict__ arena, uint32_t n, const uint8_t* __restrict__ arity,
-                              uint32_t* __restrict__ list, uint32_t* __restrict__ count) {
+                              uint32_t* __restrict__ list, uint32_t* __restrict__ count, uint32_t rich) {
     for (uint32_t base = blockIdx.x * blockDim.x; base < n; base += gridDim.x * blockDim.x) {
         uint32_t i = base + threadIdx.x;
         bool push = false;
@@ -100,7 +101,8 @@ __global__ void load_frontier(uint32_t* __restrict__ arena, uint32_t n, const ui
             uint32_t off = 0;
             if (lane == 0) off = atomicAdd(count, __popc(mask));
             off = __shfl_sync(0xffffffffu, off, 0);
-            if (push) {
+            if (push && !rich) list[off + __popc(mask & ((1u << lane) - 1))] = i;
+            if (push && rich) {
                 // rich entry with payload (sweep.cuh): slot, head, flag, args
                 uint32_t* E = list + (size_t)(off + __popc(mask & ((1u << lane) - 1))) * W;
                 const uint32_t* R = arena + (size_t)i * W;
@@ -169,6 +171,7 @@ struct trs_gpu_engine {
     std::vector<uint32_t> arity;
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
+    uint32_t rich = 0;  // frontier entry format of the loaded store (fixed at load time)
 
     // store
     uint64_t capacity = 0;        // logical capacity (slots) the step loop may use
@@ -530,6 +533,7 @@ Params make_params(trs_gpu_engine* e, int blocks) {
     P.capacity = e->capacity;
     P.max_new = e->max_new;
     P.step_budget = 1000000000ull;
+    P.rich = e->rich;
     // slab: 256 slots per warp unless the arena is small
     uint64_t per_warp = e->capacity / (4ull * (uint64_t)blocks * kWarps);
     P.slab = (uint32_t)std::max<uint64_t>(16, std::min<uint64_t>(256, per_warp));
@@ -566,7 +570,7 @@ void launch_load(trs_gpu_engine* e, uint32_t n, const uint32_t* hss, const uint3
                  const uint32_t* rc, const uint8_t* d_arity, uint32_t* count) {
     int blocks = std::max(1, std::min<int>((int)((n + 255) / 256), e->sm_count * 8));
     load_records<W><<<blocks, 256, 0, e->stream>>>(e->d_arena[0], n, hss, args, max_arity, rc);
-    load_frontier<W><<<blocks, 256, 0, e->stream>>>(e->d_arena[0], n, d_arity, e->d_list[0], count);
+    load_frontier<W><<<blocks, 256, 0, e->stream>>>(e->d_arena[0], n, d_arity, e->d_list[0], count, e->rich);
 }
 
 int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num_roots,
@@ -694,6 +698,8 @@ int trs_gpu_open(int device, trs_gpu_engine** out) {
         return TRS_GPU_CUDA;
     }
     cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
+    // experimental frontier format (sweep.cuh, rich entries); off by default
+    if (const char* r = std::getenv("TRS_B200_RICH_ENTRIES")) e->rich = std::atoi(r) ? 1u : 0u;
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
     if (!coop || cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {

@@ -128,7 +128,8 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
     }
     const uint32_t* Lin = P.list[cur];
     uint32_t* Lout = P.list[cur ^ 1];
-    for (uint32_t v = tid; v < in.M; v += nthreads) {
+    for (uint32_t v = tid; v < in.M && !P.rich; v += nthreads) Lout[v] = __ldcg(P.gcmap + Lin[frontier_phys(in, v)]);
+    for (uint32_t v = tid; v < in.M && P.rich; v += nthreads) {
         // rich entries (sweep.cuh): remap the slot and, with a payload, its arguments
         const uint32_t* E = Lin + (size_t)frontier_phys(in, v) * W;
         uint32_t* D = Lout + (size_t)v * W;

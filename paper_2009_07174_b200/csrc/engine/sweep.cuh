@@ -599,7 +599,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         return;
     }
     const uint32_t* gin = P.list[L.cur];
-    for (uint32_t v = threadIdx.x; v < F.M; v += kBlock) slist[v] = gin[(size_t)frontier_phys(F, v) * W];
+    const uint32_t stride = P.rich ? W : 1;
+    for (uint32_t v = threadIdx.x; v < F.M; v += kBlock) slist[v] = gin[(size_t)frontier_phys(F, v) * stride];
     if (threadIdx.x == 0) {
         ss.count[0] = F.M;
         ss.sc = 0;
@@ -664,8 +665,12 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     // hand the frontier back to the grid as one region of the global list
     const uint32_t m = ss.count[ss.sc];
     uint32_t* gout = P.list[L.cur];
-    for (uint32_t v = threadIdx.x; v < m; v += kBlock)
-        *reinterpret_cast<uint4*>(gout + (size_t)v * W) = make_uint4(slist[ss.sc * kSmallCap + v], 0u, 0u, 0u);
+    for (uint32_t v = threadIdx.x; v < m; v += kBlock) {
+        if (P.rich)
+            *reinterpret_cast<uint4*>(gout + (size_t)v * W) = make_uint4(slist[ss.sc * kSmallCap + v], 0u, 0u, 0u);
+        else
+            gout[v] = slist[ss.sc * kSmallCap + v];
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         region_off(P, L.cur)[0] = 0;
@@ -799,10 +804,13 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks);
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
-        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * W, &s_push, nullptr};
+        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr};
         PhaseClock pc;
-        unsigned long long rw = cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x,
-                                                     nblocks, slab, P.profile && leader, pc);
+        unsigned long long rw =
+            P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
+                                          P.profile && leader, pc)
+                   : cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
+                                           P.profile && leader, pc);
         rw = block_sum64(rw, sm);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
