@@ -1,0 +1,28 @@
+"""Profiling target: one warm run, then the profiled run of the same batch.
+
+    ncu -k regex:step_loop -s 1 -c 1 ... python tools/profile_target.py fibbatch
+
+The arena is pre-sized so each run is exactly one step-loop launch (no
+growth relaunch), so `-s 1 -c 1` captures the second, steady-state run.
+"""
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+from paper_2009_07174_b200 import api  # noqa: E402
+from tools.run_config import texts_for  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "fibbatch"
+capacity = int(sys.argv[2]) if len(sys.argv) > 2 else 128 << 20
+systems = [api.System(t) for t in texts_for(name)]
+store = api.Store.load(systems)
+eng = api.Engine(0)
+eng.set_program(systems[0])
+for rep in range(2):
+    eng.load(store, capacity=capacity)
+    st = eng.run()
+    print(json.dumps({"rep": rep, "kernel_ms": st["kernel_ms"], "launches": st["launches"], "regrows": st["regrows"],
+                      "sweeps": st["sweeps"], "rewrites": st["total_rewrites"]}), flush=True)
