@@ -506,6 +506,15 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     return TRS_GPU_OK;
 }
 
+// Host reads/writes of the control block use synchronous copies on the
+// legacy stream, which does not order against the engine's non-blocking
+// stream: drain the engine stream first at every entry point.
+int drain(trs_gpu_engine* e) {
+    cudaError_t err = cudaStreamSynchronize(e->stream);
+    if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("engine stream: ") + cudaGetErrorString(err));
+    return TRS_GPU_OK;
+}
+
 // Before every step-loop launch: barrier counter and rotating claim
 // counters start at zero.
 void reset_barrier(trs_gpu_engine* e) {
@@ -766,6 +775,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     if (!e) return TRS_GPU_INVALID;
     if (!e->loaded) return fail(e, TRS_GPU_INVALID, "no store loaded");
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     trs_gpu_options opt{};
     if (opt_in) opt = *opt_in;
     e->last_error.clear();
@@ -915,6 +925,8 @@ void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr;
 
 int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out6) {
     if (!e || !e->d_ctl || !out6) return TRS_GPU_INVALID;
+    cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     for (int k = 0; k < 6; ++k) out6[k] = c.prof[k];
@@ -924,6 +936,7 @@ int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out6) {
 int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats) {
     if (!e || !e->loaded) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     Ctl c0;
     CUDA_TRY(e, cudaMemcpy(&c0, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     const int blocks = grid_blocks(e, 0);
@@ -965,6 +978,7 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
 int trs_gpu_overhead_probe(trs_gpu_engine* e, uint32_t iters, uint32_t mode, uint32_t max_blocks, double* ns_per_iter) {
     if (!e || !e->loaded || !ns_per_iter) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     int blocks = grid_blocks(e, 0);
     if (max_blocks && (int)max_blocks < blocks) blocks = (int)max_blocks;
     Params P = make_params(e, blocks);
@@ -1002,6 +1016,7 @@ int trs_gpu_fetch_records(trs_gpu_engine* e, void* dst, uint64_t cap_bytes, uint
 int trs_gpu_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count) {
     if (!e || !e->d_trace) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     uint64_t n = std::min<uint64_t>(e->last_sweeps, e->trace_cap);
     if (count) *count = n;
     if (out && cap) CUDA_TRY(e, cudaMemcpy(out, e->d_trace, sizeof(trs_gpu_sweep_record) * std::min(n, cap), cudaMemcpyDeviceToHost));
@@ -1013,6 +1028,7 @@ int trs_gpu_canonical(trs_gpu_engine* e, uint32_t root_index, uint32_t* words, u
     if (!e || !e->loaded) return TRS_GPU_INVALID;
     if (root_index >= e->num_roots) return fail(e, TRS_GPU_INVALID, "root index out of range");
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     HostArena h;
     std::vector<uint32_t> roots;
     int rc = fetch_arena(e, h, roots);
@@ -1060,6 +1076,7 @@ int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uin
                         uint32_t* refcounts, uint8_t* nf, uint32_t cap) {
     if (!e || !e->loaded || !n) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
     HostArena h;
     std::vector<uint32_t> roots;
     int rc = fetch_arena(e, h, roots);
