@@ -115,7 +115,7 @@ typedef struct trs_gpu_options {
     uint32_t blocks_per_sm;    /* 0 -> occupancy maximum */
     uint32_t variant;          /* step-loop register budget: 0/1 = 1 CTA/SM no spills, 2 = 2 CTAs/SM */
     uint32_t max_blocks;       /* >0: cap the persistent grid (profiling the single-CTA mode) */
-    uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters) */
+    uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters); >1: only grid sweeps of <= profile entries */
     uint32_t disable_warp_mode; /* 1: frontiers <= 32 slots still run on the whole CTA */
     uint32_t reserved[4];
 } trs_gpu_options;
@@ -214,7 +214,7 @@ void* trs_gpu_stream(trs_gpu_engine* engine);
 
 /* Debug phase counters of the last runs (cycles summed over sweeps of CTA
  * 0's thread 0): match, claim, apply, push, whole single-CTA sweep, sweeps. */
-int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out6);
+int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out12);
 
 /* Fixed per-sweep overhead probe on the loaded store: `iters` grid barriers
  * (mode 0) or barriers plus the frontier-table staging of a grid sweep
@@ -235,9 +235,10 @@ int trs_gpu_fetch_records(trs_gpu_engine* engine, void* dst, uint64_t cap_bytes,
                           uint32_t* record_words, uint32_t* roots_out);
 
 /* Device-side roofline probe: `iters` launches of a uniformly random 4-byte
- * (bytes_per_access = 4), 8-byte or 16-byte gather over a `bytes`-sized
- * array in HBM (indices streamed coalesced).  Returns achieved GB/s counting
- * bytes_per_access per access. */
+ * (bytes_per_access = 4), 8-, 16- or 32-byte gather over a power-of-two array
+ * of at most `bytes` in HBM (indices streamed coalesced, 4 independent
+ * gathers in flight per thread, a full SM of threads).  Returns achieved GB/s
+ * counting bytes_per_access per access. */
 int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters,
                          double* gbps);
 

@@ -23,7 +23,9 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtrs_b200.so")
+# TRS_B200_PROFILE_BUILD=1 selects the profiling build (phase cycle counters)
+LIB_PATH = os.path.join(_HERE, "libtrs_b200_prof.so" if os.environ.get("TRS_B200_PROFILE_BUILD") == "1"
+                        else "libtrs_b200.so")
 
 OK, STEP_BUDGET, CAPACITY, DANGLING, INVALID, CUDA = range(6)
 
@@ -445,9 +447,10 @@ class Engine:
         return ns.value
 
     def profile_counters(self) -> dict:
-        out = np.zeros(6, np.uint64)
+        out = np.zeros(12, np.uint64)
         lib().trs_gpu_profile_counters(self._h, out.ctypes.data)
-        keys = ("match", "claim", "apply", "push", "sweep", "sweeps")
+        keys = ("match", "claim", "apply", "push", "sweep", "sweeps", "steps", "spare",
+                "m_record", "m_children", "m_slots", "m_rules")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def compact(self, max_rounds: int = 8) -> dict:

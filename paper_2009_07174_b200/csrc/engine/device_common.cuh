@@ -51,8 +51,10 @@ struct Ctl {
     // frontier layout: list buffer b holds nregions[b] regions whose
     // (offset, count) pairs live in Params::regions
     uint32_t nregions[2];
-    // phase cycle accounting (Params::profile): match, claim, apply, push, sweep, sweeps
-    unsigned long long prof[6];
+    // phase cycle accounting (Params::profile): match, claim, apply, push,
+    // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
+    // the match sub-phases: record, children, slots, rules
+    unsigned long long prof[12];
 };
 
 struct Params {
@@ -80,7 +82,7 @@ struct Params {
     uint32_t sweep0;        // sweeps completed before this run (epochs keep counting)
     uint32_t compact_only;  // >0: run at most this many compaction rounds and exit
     uint32_t prefer_grow;   // out of headroom: grow (host) rather than collect
-    uint32_t profile;       // phase cycle accounting of CTA 0 (debug)
+    uint32_t profile;       // phase cycle accounting of CTA 0 (debug): 1 every sweep, >1 grid sweeps of <= profile entries
     uint32_t slab;          // fresh slots a warp claims at a time
     uint32_t probe_iters;   // >0: time this many grid barriers and exit (trs_gpu_overhead_probe)
     uint32_t probe_mode;
@@ -203,6 +205,7 @@ struct Prog {
     const DStep* steps;
     const DInstr* instrs;
     const uint16_t* refs;
+    const DPlan* plans;
     uint32_t max_new;
 };
 
@@ -215,6 +218,7 @@ __device__ __forceinline__ Prog view_prog(const uint8_t* blob) {
     p.steps = reinterpret_cast<const DStep*>(blob + h->off_steps);
     p.instrs = reinterpret_cast<const DInstr*>(blob + h->off_instrs);
     p.refs = reinterpret_cast<const uint16_t*>(blob + h->off_refs);
+    p.plans = reinterpret_cast<const DPlan*>(blob + h->off_plans);
     p.max_new = h->max_new_slots;
     return p;
 }
@@ -235,9 +239,9 @@ __device__ __forceinline__ uint32_t* rec(uint32_t* arena, uint32_t i) {
 
 // Load the first `ar` argument words of a record (whole 16-byte quads).
 template <int W>
-__device__ __forceinline__ void load_args(const uint32_t* r, uint32_t ar, uint32_t (&a)[W - 4]) {
+__device__ __forceinline__ void load_args(const uint32_t* r, uint32_t ar, uint32_t (&a)[rec_args(W)]) {
 #pragma unroll
-    for (int q = 0; q < (W - 4) / 4; ++q) {
+    for (int q = 0; q < rec_args(W) / 4; ++q) {
         if ((uint32_t)(q * 4) < ar) {
             uint4 v = *reinterpret_cast<const uint4*>(r + kWArgs + q * 4);
             a[q * 4 + 0] = v.x;
@@ -251,9 +255,9 @@ __device__ __forceinline__ void load_args(const uint32_t* r, uint32_t ar, uint32
 }
 
 template <int W>
-__device__ __forceinline__ void store_args(uint32_t* r, const uint32_t (&a)[W - 4], uint32_t ar) {
+__device__ __forceinline__ void store_args(uint32_t* r, const uint32_t (&a)[rec_args(W)], uint32_t ar) {
 #pragma unroll
-    for (int q = 0; q < (W - 4) / 4; ++q) {
+    for (int q = 0; q < rec_args(W) / 4; ++q) {
         if ((uint32_t)(q * 4) < ar || q == 0) {
             *reinterpret_cast<uint4*>(r + kWArgs + q * 4) =
                 make_uint4(a[q * 4 + 0], a[q * 4 + 1], a[q * 4 + 2], a[q * 4 + 3]);
@@ -261,16 +265,26 @@ __device__ __forceinline__ void store_args(uint32_t* r, const uint32_t (&a)[W - 
     }
 }
 
-// Entries of a sweep are handed out in 32-entry chunks round-robin over all
-// warps of the participating CTAs, so CTA b of n processes exactly
-// cta_entries(b) of m entries and the entries of CTAs < b number
+// Entries of a sweep are handed out in chunks of q <= 32 entries (one per
+// lane), round-robin over all warps of the participating CTAs.  q is the
+// smallest chunk that covers the frontier in one round, so a medium sweep
+// spreads over every warp of the grid: fewer lanes per warp means fewer
+// divergent symbol/rule paths in each warp's instruction stream, which is
+// what bounds a sweep that is one chunk deep.  CTA b of n then processes
+// exactly cta_entries(b) of m entries and the entries of CTAs < b number
 // cta_prefix(b); its next-frontier pushes (at most max_new + 1 per entry)
 // therefore fit the output region [(max_new+1) * prefix, +(max_new+1) * count).
-__device__ __forceinline__ uint32_t cta_prefix(uint32_t m, uint32_t b, uint32_t nblocks) {
-    const uint64_t round = (uint64_t)nblocks * kBlock;
+__device__ __forceinline__ uint32_t chunk_lanes(uint32_t m, uint32_t nblocks) {
+    const uint32_t gw = nblocks * kWarps;
+    const uint32_t q = (m + gw - 1) / gw;
+    return q < 1 ? 1 : q > 32 ? 32 : q;
+}
+
+__device__ __forceinline__ uint32_t cta_prefix(uint32_t m, uint32_t b, uint32_t nblocks, uint32_t q) {
+    const uint64_t round = (uint64_t)nblocks * kWarps * q;
     const uint64_t full = m / round;
     const uint64_t rem = m - full * round;
-    const uint64_t before = (uint64_t)b * kBlock;
+    const uint64_t before = (uint64_t)b * kWarps * q;
     return (uint32_t)(full * before + (rem < before ? rem : before));
 }
 

@@ -37,6 +37,14 @@ constexpr uint32_t kMaxProgramBytes = 40 * 1024;
 //   w4.. arguments
 constexpr uint32_t kWHead = 0, kWEpoch = 1, kWRc = 2, kWWaiter = 3, kWArgs = 4;
 
+// Arguments a W-word record carries.  W = 16 holds at most 8 (not 12): the
+// step loop keeps per-argument state in registers, and arity 9-12 systems
+// are rare enough to take the 32-word layout instead.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr int rec_args(int W) { return W == 16 ? 8 : W - 4; }
+
 struct DRule {
     uint16_t first_step;
     uint8_t num_steps;
@@ -48,7 +56,8 @@ struct DRule {
     uint8_t collapse;
     uint8_t root_wait;   // fresh instr the rewritten root sleeps on (kNone: push root)
     uint8_t root_cursor; // argument position of that wait
-    uint8_t pad[3];
+    uint8_t csrc;        // collapse source already in registers (kSrc* code of its binding step) or kNone
+    uint8_t pad[2];
     uint32_t push_mask;  // bit k: fresh instr k goes on the next frontier list
 };
 static_assert(sizeof(DRule) == 20, "DRule layout");
@@ -57,7 +66,7 @@ struct DStep {
     uint8_t kind;  // 0 CheckHead, 1 BindVar
     uint8_t child;
     int8_t parent; // step index within the rule, -1 = redex root
-    uint8_t pad;
+    uint8_t src;   // where the level-synchronous matcher finds the value (kSrc*), see DPlan
     uint32_t value;
 };
 static_assert(sizeof(DStep) == 8, "DStep layout");
@@ -74,6 +83,37 @@ static_assert(sizeof(DInstr) == 12, "DInstr layout");
 
 constexpr uint16_t kRefNode = 0x8000;
 
+// Level-synchronous matching plan of one symbol.  The interpreted matcher
+// walks each rule's steps in order (run_match_program, dispatch.hpp:95-117),
+// one dependent gather per step below the root, and lanes of a warp trying
+// different rules serialise those chains.  With a plan every lane instead
+// issues the same loads at the same point: level 1 the redex's children
+// (head, nf epoch and -- for the first kPlanChildren children, when listed
+// in `child_args` -- their first four arguments, all in the child's first
+// sector), level 2 the records of up to kPlanSlots grandchildren `slot_jk`
+// (= child j's argument k), of which the first kPlanArgSlots may also bring
+// their arguments.  (The limits keep the matcher's registers below the
+// occupancy budget; they cover every pattern of the BASELINE systems.)  Every step of every rule of the
+// symbol then reads its value from registers (DStep::src):
+//   CheckHead  kSrcChild + c   head of child c
+//              kSrcSlot + s    head of slot s
+//   BindVar    kSrcChild + c   child c (the redex's argument)
+//              kSrcCArg + 4j+k argument k of child j
+//              kSrcSArg + 4s+k argument k of slot s
+// Symbols whose rules reach deeper (or past these limits) keep the
+// interpreted matcher (fast = 0).
+constexpr uint8_t kSrcChild = 0x00, kSrcSlot = 0x40, kSrcCArg = 0x80, kSrcSArg = 0xC0;
+constexpr uint32_t kPlanSlots = 2, kPlanArgSlots = 1, kPlanChildren = 2;
+
+struct DPlan {
+    uint8_t fast;
+    uint8_t child_args;  // bit j: load child j's first argument quad
+    uint8_t nslots;
+    uint8_t slot_args;   // bit s (s < kPlanArgSlots): load slot s's first argument quad
+    uint8_t slot_jk[4];
+};
+static_assert(sizeof(DPlan) == 8, "DPlan layout");
+
 struct ProgHeader {
     uint32_t num_symbols;
     uint32_t num_rules;
@@ -88,6 +128,7 @@ struct ProgHeader {
     uint32_t off_steps;       // DStep[]
     uint32_t off_instrs;      // DInstr[]
     uint32_t off_refs;        // uint16_t[]
+    uint32_t off_plans;       // DPlan[num_symbols]
     uint32_t bytes;           // total blob size (multiple of 16)
 };
 

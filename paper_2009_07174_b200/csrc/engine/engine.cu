@@ -66,7 +66,7 @@ __global__ void load_records(uint32_t* __restrict__ arena, uint32_t n, const uin
         if (i != 0) {
             w[kWHead] = hss[i];
             w[kWRc] = rc[i];
-            for (uint32_t j = 0; j < max_arity && j < (uint32_t)(W - 4); ++j)
+            for (uint32_t j = 0; j < max_arity && j < (uint32_t)rec_args(W); ++j)
                 w[kWArgs + j] = args[(size_t)j * n + i];
         } else {
             w[kWEpoch] = 1;  // slot 0 is never a term; keep it inert
@@ -124,19 +124,41 @@ __global__ void init_ctl(Ctl* ctl, uint32_t* regions, const uint32_t* count, uin
     regions[kMaxGrid] = *count;      // buffer 0, count of region 0
 }
 
-__global__ void gather_probe_kernel(const uint32_t* __restrict__ data, uint64_t words, const uint32_t* __restrict__ idx,
-                                    uint32_t n, uint32_t vec, uint32_t* __restrict__ sink) {
+// Random-gather roofline: uniformly random VEC-word accesses over a
+// power-of-two array far larger than L2, indices streamed coalesced.  Each
+// thread keeps kProbeILP independent gathers in flight (the engine's warp
+// step issues its child probes together the same way), and addressing is a
+// mask, so the probe is bound by the memory system, not by issue.
+constexpr int kProbeILP = 4;
+template <int VEC>
+__global__ void __launch_bounds__(512) gather_probe_kernel(const uint32_t* __restrict__ data, uint64_t mask,
+                                                           const uint32_t* __restrict__ idx, uint32_t n,
+                                                           uint32_t* __restrict__ sink) {
     uint32_t acc = 0;
-    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
-        uint64_t e = idx[k];
-        if (vec == 1) {
-            acc += data[e % words];
-        } else if (vec == 2) {
-            uint2 v = reinterpret_cast<const uint2*>(data)[e % (words / 2)];
-            acc += v.x ^ v.y;
-        } else {
-            uint4 v = reinterpret_cast<const uint4*>(data)[e % (words / 4)];
-            acc += v.x ^ v.y ^ v.z ^ v.w;
+    const uint32_t stride = gridDim.x * blockDim.x;
+    for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += stride * kProbeILP) {
+        uint32_t e[kProbeILP];
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) {
+            const uint32_t kk = k + (uint32_t)u * stride;
+            e[u] = kk < n ? __ldcs(idx + kk) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < kProbeILP; ++u) {
+            const uint64_t w = ((uint64_t)e[u] * VEC) & mask;
+            if (VEC == 1) {
+                acc += data[w];
+            } else if (VEC == 2) {
+                const uint2 v = *reinterpret_cast<const uint2*>(data + w);
+                acc += v.x ^ v.y;
+            } else if (VEC == 4) {
+                const uint4 v = *reinterpret_cast<const uint4*>(data + w);
+                acc += v.x ^ v.y ^ v.z ^ v.w;
+            } else {
+                const uint4 v = *reinterpret_cast<const uint4*>(data + w);
+                const uint4 x = *reinterpret_cast<const uint4*>(data + w + 4);
+                acc += v.x ^ v.y ^ v.z ^ v.w ^ x.x ^ x.y ^ x.z ^ x.w;
+            }
         }
     }
     if (acc == 0x9e3779b9u) sink[0] = acc;
@@ -237,12 +259,143 @@ void free_store(trs_gpu_engine* e) {
 
 int words_for_arity(uint32_t max_arity) {
     if (max_arity <= 4) return 8;
-    if (max_arity <= 12) return 16;
+    if (max_arity <= 8) return 16;
     if (max_arity <= 28) return 32;
     return 0;
 }
 
 // Build the device blob from the flattened reference DispatchTable.
+// Level-synchronous matching plan of symbol f (device_program.hpp, DPlan):
+// assigns every step of f's rules a register source and the collapse
+// source of each collapsing rule, or leaves f on the interpreted matcher.
+DPlan plan_symbol(const trs_gpu_program* p, uint32_t f, std::vector<DStep>& steps, std::vector<DRule>& rules) {
+    DPlan pl{};
+    struct Path {
+        int depth;
+        uint32_t c[3];
+    };
+    std::vector<std::pair<uint32_t, bool>> slots;  // (4j+k, needs its argument quad)
+    auto slot_of = [&](uint32_t jk, bool args) -> int {
+        for (size_t q = 0; q < slots.size(); ++q)
+            if (slots[q].first == jk) {
+                slots[q].second = slots[q].second || args;
+                return (int)q;
+            }
+        slots.push_back({jk, args});
+        return (int)slots.size() - 1;
+    };
+    bool fast = true;
+    std::vector<std::vector<Path>> paths;
+    for (uint32_t r = p->rule_begin[f]; r < p->rule_begin[f + 1]; ++r) {
+        const trs_gpu_rule& R = p->rules[r];
+        std::vector<Path> ps(R.num_steps);
+        for (uint32_t t = 0; t < R.num_steps; ++t) {
+            const trs_gpu_step& S = p->steps[R.first_step + t];
+            Path q{};
+            if (S.parent < 0) {
+                q.depth = 1;
+                q.c[0] = S.child;
+            } else {
+                q = ps[S.parent];
+                if (q.depth >= 3) {
+                    fast = false;
+                    q.depth = 4;
+                } else {
+                    q.c[q.depth++] = S.child;
+                }
+            }
+            ps[t] = q;
+            if (q.depth >= 2 && (q.c[0] >= kPlanChildren || q.c[1] >= 4)) fast = false;
+            if (q.depth == 3 && (S.kind == TRS_GPU_STEP_CHECK_HEAD || q.c[2] >= 4)) fast = false;
+            if (q.depth > 3) fast = false;
+            if (!fast) break;
+            if (q.depth == 2) {
+                pl.child_args |= (uint8_t)(1u << q.c[0]);
+                if (S.kind == TRS_GPU_STEP_CHECK_HEAD) slot_of(q.c[0] * 4 + q.c[1], false);
+            } else if (q.depth == 3) {
+                pl.child_args |= (uint8_t)(1u << q.c[0]);
+                slot_of(q.c[0] * 4 + q.c[1], true);
+            }
+        }
+        paths.push_back(std::move(ps));
+        if (!fast) break;
+    }
+    auto arg_slots = [&]() {
+        uint32_t n = 0;
+        for (auto& sl : slots) n += sl.second;
+        return n;
+    };
+    if (!fast || slots.size() > kPlanSlots || arg_slots() > kPlanArgSlots) return DPlan{};
+    // collapse sources: the record of the bound node is already in registers
+    // when it is a child (with its argument quad) or an argument slot
+    std::vector<int> csrc_slot(paths.size(), -1);
+    for (uint32_t r = p->rule_begin[f], x = 0; r < p->rule_begin[f + 1]; ++r, ++x) {
+        const trs_gpu_rule& R = p->rules[r];
+        if (R.root_ref & TRS_GPU_REF_NODE) continue;
+        int bind_t = -1;
+        for (uint32_t t = 0; t < R.num_steps; ++t) {
+            const trs_gpu_step& S = p->steps[R.first_step + t];
+            if (S.kind == TRS_GPU_STEP_BIND_VAR && S.value == R.root_ref) bind_t = (int)t;
+        }
+        if (bind_t < 0) continue;
+        const Path& q = paths[x][bind_t];
+        if (q.depth == 1 && q.c[0] < kPlanChildren) {
+            pl.child_args |= (uint8_t)(1u << q.c[0]);
+            csrc_slot[x] = -2;  // child
+        } else if (q.depth == 2) {
+            auto saved = slots;
+            int sl = slot_of(q.c[0] * 4 + q.c[1], true);
+            if (slots.size() > kPlanSlots || arg_slots() > kPlanArgSlots) {
+                slots = saved;
+            } else {
+                csrc_slot[x] = sl;
+            }
+        }
+    }
+    // argument-carrying slots first: only the first kPlanArgSlots may load arguments
+    std::vector<int> order(slots.size());
+    for (size_t q = 0; q < order.size(); ++q) order[q] = (int)q;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return slots[x].second > slots[y].second; });
+    std::vector<int> rank(slots.size());
+    for (size_t q = 0; q < order.size(); ++q) rank[order[q]] = (int)q;
+    pl.fast = 1;
+    pl.nslots = (uint8_t)slots.size();
+    for (size_t q = 0; q < slots.size(); ++q) {
+        pl.slot_jk[rank[q]] = (uint8_t)slots[q].first;
+        if (slots[q].second) pl.slot_args |= (uint8_t)(1u << rank[q]);
+    }
+    auto find_slot = [&](uint32_t jk) {
+        for (size_t q = 0; q < slots.size(); ++q)
+            if (slots[q].first == jk) return rank[q];
+        return -1;
+    };
+    for (uint32_t r = p->rule_begin[f], x = 0; r < p->rule_begin[f + 1]; ++r, ++x) {
+        const trs_gpu_rule& R = p->rules[r];
+        for (uint32_t t = 0; t < R.num_steps; ++t) {
+            const trs_gpu_step& S = p->steps[R.first_step + t];
+            const Path& q = paths[x][t];
+            uint8_t src;
+            if (q.depth == 1)
+                src = (uint8_t)(kSrcChild + q.c[0]);
+            else if (q.depth == 2)
+                src = S.kind == TRS_GPU_STEP_CHECK_HEAD ? (uint8_t)(kSrcSlot + find_slot(q.c[0] * 4 + q.c[1]))
+                                                       : (uint8_t)(kSrcCArg + q.c[0] * 4 + q.c[1]);
+            else
+                src = (uint8_t)(kSrcSArg + find_slot(q.c[0] * 4 + q.c[1]) * 4 + q.c[2]);
+            steps[R.first_step + t].src = src;
+        }
+        if (csrc_slot[x] == -2) {
+            for (uint32_t t = 0; t < R.num_steps; ++t) {
+                const trs_gpu_step& S = p->steps[R.first_step + t];
+                if (S.kind == TRS_GPU_STEP_BIND_VAR && S.value == R.root_ref) rules[r].csrc = (uint8_t)(kSrcChild + paths[x][t].c[0]);
+            }
+        } else if (csrc_slot[x] >= 0) {
+            rules[r].csrc = (uint8_t)(kSrcSlot + rank[csrc_slot[x]]);
+        }
+    }
+    return pl;
+}
+
 int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!p || !p->arity || !p->rule_begin) return fail(e, TRS_GPU_INVALID, "null program");
     if (p->num_symbols == 0 || p->num_symbols > (1u << 16) - 2)
@@ -281,6 +434,7 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
         D.new_slots = collapse ? 0 : (uint8_t)(R.num_instrs - 1);
         D.root_wait = kNone;
         D.root_cursor = 0;
+        D.csrc = kNone;
         max_new = std::max<uint32_t>(max_new, D.new_slots);
         for (uint32_t t = 0; t < R.num_steps; ++t) {
             const trs_gpu_step& S = p->steps[R.first_step + t];
@@ -291,6 +445,7 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
             if (S.kind == TRS_GPU_STEP_BIND_VAR && S.value >= R.num_vars)
                 return fail(e, TRS_GPU_INVALID, "bind var slot out of range");
             d.kind = (uint8_t)S.kind;
+            d.src = kNone;
             d.child = (uint8_t)S.child;
             d.parent = (int8_t)S.parent;
             d.value = S.value;
@@ -342,6 +497,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
             }
         }
     }
+    std::vector<DPlan> plans(p->num_symbols);
+    for (uint32_t f = 0; f < p->num_symbols; ++f) plans[f] = plan_symbol(p, f, steps, rules);
     for (uint32_t k = 0; k < p->num_refs; ++k) {
         uint32_t ref = p->refs[k];
         refs[k] = (ref & TRS_GPU_REF_NODE) ? (uint16_t)(kRefNode | (ref & 0x7fff)) : (uint16_t)ref;
@@ -369,6 +526,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     off = align16(off + sizeof(DInstr) * p->num_instrs);
     h.off_refs = off;
     off = align16(off + 2 * p->num_refs);
+    h.off_plans = off;
+    off = align16(off + sizeof(DPlan) * p->num_symbols);
     h.bytes = off;
     if (h.bytes > kMaxProgramBytes) return fail(e, TRS_GPU_INVALID, "program blob above 40 KiB");
     std::vector<uint8_t> blob(h.bytes, 0);
@@ -383,6 +542,7 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!steps.empty()) std::memcpy(blob.data() + h.off_steps, steps.data(), sizeof(DStep) * steps.size());
     if (!instrs.empty()) std::memcpy(blob.data() + h.off_instrs, instrs.data(), sizeof(DInstr) * instrs.size());
     if (!refs.empty()) std::memcpy(blob.data() + h.off_refs, refs.data(), 2 * refs.size());
+    std::memcpy(blob.data() + h.off_plans, plans.data(), sizeof(DPlan) * plans.size());
     e->blob = std::move(blob);
     e->max_arity = max_arity;
     e->max_new = max_new;
@@ -587,7 +747,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
               uint64_t capacity) {
     if (e->blob.empty()) return fail(e, TRS_GPU_INVALID, "no program set");
     if (n < 2 || num_roots == 0) return fail(e, TRS_GPU_INVALID, "empty store");
-    if (max_arity > (uint32_t)(e->W - 4))
+    if (max_arity > (uint32_t)rec_args(e->W))
         return fail(e, TRS_GPU_INVALID, "store arity exceeds program record width");
     for (uint32_t r = 0; r < num_roots; ++r)
         if (roots[r] == 0 || roots[r] >= n) return fail(e, TRS_GPU_INVALID, "root out of range");
@@ -923,13 +1083,13 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
 
 void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr; }
 
-int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out6) {
-    if (!e || !e->d_ctl || !out6) return TRS_GPU_INVALID;
+int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out12) {
+    if (!e || !e->d_ctl || !out12) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
-    for (int k = 0; k < 6; ++k) out6[k] = c.prof[k];
+    for (int k = 0; k < 12; ++k) out12[k] = c.prof[k];
     return TRS_GPU_OK;
 }
 
@@ -1113,10 +1273,12 @@ int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uin
 }
 
 int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters, double* gbps) {
-    if (!gbps || (bytes_per_access != 4 && bytes_per_access != 8 && bytes_per_access != 16)) return TRS_GPU_INVALID;
+    if (!gbps || (bytes_per_access != 4 && bytes_per_access != 8 && bytes_per_access != 16 && bytes_per_access != 32))
+        return TRS_GPU_INVALID;
     if (cudaSetDevice(device) != cudaSuccess) return TRS_GPU_CUDA;
-    uint64_t words = bytes / 4;
-    const uint32_t n = 1u << 28;  // accesses per launch
+    uint64_t words = 1;
+    while (words * 2 <= bytes / 4) words *= 2;  // power of two: addressing is a mask
+    const uint32_t n = 1u << 28;                // accesses per launch
     uint32_t *data = nullptr, *idx = nullptr, *sink = nullptr;
     if (cudaMalloc(&data, words * 4) != cudaSuccess) return TRS_GPU_CUDA;
     if (cudaMalloc(&idx, (size_t)n * 4) != cudaSuccess || cudaMalloc(&sink, 4) != cudaSuccess) {
@@ -1128,13 +1290,23 @@ int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, 
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
     fill_random<<<sms * 8, 256>>>(idx, n, 12345);
-    uint32_t vec = bytes_per_access / 4;
-    gather_probe_kernel<<<sms * 8, 512>>>(data, words, idx, n, vec, sink);  // warm-up
+    const uint32_t vec = bytes_per_access / 4;
+    const uint64_t mask = (words - 1) & ~(uint64_t)(vec - 1);
+    auto launch = [&]() {
+        const int grid = sms * 4;  // 4 x 512 threads = a full SM
+        switch (vec) {
+            case 1: gather_probe_kernel<1><<<grid, 512>>>(data, mask, idx, n, sink); break;
+            case 2: gather_probe_kernel<2><<<grid, 512>>>(data, mask, idx, n, sink); break;
+            case 4: gather_probe_kernel<4><<<grid, 512>>>(data, mask, idx, n, sink); break;
+            default: gather_probe_kernel<8><<<grid, 512>>>(data, mask, idx, n, sink); break;
+        }
+    };
+    launch();  // warm-up
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     cudaEventRecord(a);
-    for (uint32_t k = 0; k < iters; ++k) gather_probe_kernel<<<sms * 8, 512>>>(data, words, idx, n, vec, sink);
+    for (uint32_t k = 0; k < iters; ++k) launch();
     cudaEventRecord(b);
     cudaError_t err = cudaEventSynchronize(b);
     float ms = 0;

@@ -41,8 +41,27 @@ struct StepCtx {
     uint32_t* abort_flag; // shared flag raised with ctl->abort_capacity (may be null)
 };
 
+// Phase cycle accounting is compiled only into the profiling build
+// (libtrs_b200_prof.so, -DTRS_B200_PROFILE=1) so that the production step
+// loop carries none of its registers.
+#ifndef TRS_B200_PROFILE
+#define TRS_B200_PROFILE 0
+#endif
+constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
+
 struct PhaseClock {
     long long t[4] = {0, 0, 0, 0};  // match, claim, apply, push (debug accounting)
+    long long steps = 0;            // warp steps accounted
+    long long sub[4] = {0, 0, 0, 0};  // match sub-phases: entry+record, children, slots, rules
+    long long last = 0;
+    // close a sub-phase once value v has arrived (the MOV waits on its scoreboard)
+    __device__ __forceinline__ void mark(int k, uint32_t v) {
+        uint32_t d;
+        asm volatile("mov.b32 %0, %1;" : "=r"(d) : "r"(v));
+        long long now = clock64() + (d & 0);
+        sub[k] += now - last;
+        last = now;
+    }
 };
 
 // One entry per lane: derive (sweep_engine.cpp:163-188), claim, apply
@@ -58,16 +77,30 @@ constexpr uint32_t kEntHasPayload = 1;
 
 template <int W, bool kRich>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
-                                              Slab& slab, bool valid, const uint32_t* entry, bool prof,
+                                              Slab& slab, bool valid, const uint32_t* entry, bool prof_req,
                                               PhaseClock& pc) {
-    constexpr int MAXA = W - 4;
+    const bool prof = kProfBuild && prof_req;
+    constexpr int MAXA = rec_args(W);
     const uint32_t s = C.s;
     const uint32_t lane = threadIdx.x & 31;
     long long c0 = prof ? clock64() : 0;
+    if (prof) {
+        pc.steps++;
+        pc.last = c0;
+    }
     uint32_t act = kActNone;
     uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
     uint32_t a[MAXA];
     uint32_t bind[kMaxVars];
+    // level-synchronous matcher state (DPlan): children's first argument
+    // quads, grandchild slot heads, and the argument quads of two slots
+    uint32_t ch[MAXA];
+    uint32_t ca[kPlanChildren * 4];
+    uint32_t gh[kPlanSlots];
+    uint32_t ga[kPlanArgSlots * 4];
+    uint32_t cs_head = 0, cs_b[4] = {0, 0, 0, 0};  // collapse source record taken from registers
+    uint32_t own_waiter = 0;  // the record's waiter word as loaded (the nf publication's first guess)
+    bool planned = false;
     if (valid) {
         uint32_t headw;
         bool have = false;
@@ -90,26 +123,65 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             i = *entry;
         }
         if (!have) {
-            uint32_t* R = rec<W>(arena, i);
-            headw = R[kWHead];
-            load_args<W>(R, G.arity[headw & kSymMask], a);
+            // head and the first argument quad share the record's first
+            // sector: issue both loads together
+            const uint32_t* R = rec<W>(arena, i);
+            const uint4 h4 = *reinterpret_cast<const uint4*>(R);
+            const uint4 a4 = *reinterpret_cast<const uint4*>(R + kWArgs);
+            headw = h4.x;
+            own_waiter = h4.w;
+            a[0] = a4.x;
+            a[1] = a4.y;
+            a[2] = a4.z;
+            a[3] = a4.w;
+            const uint32_t har = G.arity[headw & kSymMask];
+#pragma unroll
+            for (int q = 1; q < MAXA / 4; ++q) {
+                if ((uint32_t)(q * 4) < har) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(R + kWArgs + q * 4);
+                    a[q * 4 + 0] = v.x;
+                    a[q * 4 + 1] = v.y;
+                    a[q * 4 + 2] = v.z;
+                    a[q * 4 + 3] = v.w;
+                } else {
+                    a[q * 4 + 0] = a[q * 4 + 1] = a[q * 4 + 2] = a[q * 4 + 3] = 0;
+                }
+            }
         }
+        if (prof) pc.mark(0, headw ^ a[0]);
         sym = headw & kSymMask;
         cursor = headw >> kSymBits;
         ar = G.arity[sym];
-        // subterm scan (sweep_engine.cpp:173-178); all child probes issue together
-        uint32_t ch[MAXA];
+        const DPlan pl = G.plans[sym];
+        // level 1 -- subterm scan (sweep_engine.cpp:173-178): every child's
+        // head and nf epoch, plus the argument quads the plan needs, issued
+        // together
         uint32_t cep[MAXA];
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
             ch[j] = 0;
             cep[j] = 1;
             if ((uint32_t)j < ar) {
-                uint2 c = *reinterpret_cast<const uint2*>(rec<W>(arena, a[j]));
-                ch[j] = c.x & kSymMask;
-                cep[j] = c.y;
+                const uint32_t* C = rec<W>(arena, a[j]);
+                if (j < (int)kPlanChildren && ((pl.child_args >> j) & 1u)) {
+                    const uint4 q0 = *reinterpret_cast<const uint4*>(C);
+                    const uint4 q1 = *reinterpret_cast<const uint4*>(C + kWArgs);
+                    ch[j] = q0.x & kSymMask;
+                    cep[j] = q0.y;
+                    ca[j * 4 + 0] = q1.x;
+                    ca[j * 4 + 1] = q1.y;
+                    ca[j * 4 + 2] = q1.z;
+                    ca[j * 4 + 3] = q1.w;
+                } else {
+                    const uint2 c = *reinterpret_cast<const uint2*>(C);
+                    ch[j] = c.x & kSymMask;
+                    cep[j] = c.y;
+                }
             }
+            if (j < (int)kPlanChildren && !((uint32_t)j < ar && ((pl.child_args >> j) & 1u)))
+                ca[j * 4 + 0] = ca[j * 4 + 1] = ca[j * 4 + 2] = ca[j * 4 + 3] = 0;
         }
+        if (prof) pc.mark(1, cep[0] ^ cep[MAXA - 1] ^ ca[0]);
         bool pending = false;
 #pragma unroll
         for (int j = MAXA - 1; j >= 0; --j) {
@@ -122,8 +194,73 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         if (pending) {
             act = kActWait;
             wchild = pick(a, wpos);
+        } else if (pl.fast) {
+            planned = true;
+            // level 2: grandchild slots (nf below an nf child: stable)
+#pragma unroll
+            for (int q = 0; q < (int)kPlanSlots; ++q) {
+                gh[q] = 0;
+                if (q < (int)kPlanArgSlots) ga[q * 4 + 0] = ga[q * 4 + 1] = ga[q * 4 + 2] = ga[q * 4 + 3] = 0;
+                if ((uint32_t)q < pl.nslots) {
+                    const uint32_t node = pick(ca, pl.slot_jk[q]);
+                    const uint32_t* N = rec<W>(arena, node);
+                    if (q < (int)kPlanArgSlots && ((pl.slot_args >> q) & 1u)) {
+                        const uint4 q0 = *reinterpret_cast<const uint4*>(N);
+                        const uint4 q1 = *reinterpret_cast<const uint4*>(N + kWArgs);
+                        gh[q] = q0.x & kSymMask;
+                        ga[q * 4 + 0] = q1.x;
+                        ga[q * 4 + 1] = q1.y;
+                        ga[q * 4 + 2] = q1.z;
+                        ga[q * 4 + 3] = q1.w;
+                    } else {
+                        gh[q] = N[kWHead] & kSymMask;
+                    }
+                }
+            }
+            if (prof) pc.mark(2, gh[0] ^ ga[0]);
+            // first matching rule in source order (dispatch.hpp:119-130),
+            // every step answered from registers
+            int chosen = -1;
+            for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
+                const DRule& Rl = G.rules[r];
+                bool ok = true;
+                for (uint32_t t = 0; t < Rl.num_steps; ++t) {
+                    const DStep st = G.steps[Rl.first_step + t];
+                    const uint32_t src = st.src;
+                    if (st.kind == 0) {
+                        const uint32_t head = src < kSrcSlot ? pick(ch, src) : pick(gh, src & 3u);
+                        if (head != st.value) {
+                            ok = false;
+                            break;
+                        }
+                    } else {
+                        const uint32_t node = src < kSrcSlot ? pick(a, src)
+                                              : src < kSrcSArg ? pick(ca, src & 15u)
+                                                               : pick(ga, src & 7u);
+                        bind[st.value] = node;
+                    }
+                }
+                if (ok) {
+                    chosen = (int)r;
+                    break;
+                }
+            }
+            if (chosen < 0) {
+                act = kActNf;
+            } else {
+                rule = (uint32_t)chosen;
+                const DRule& Rl = G.rules[rule];
+                act = Rl.collapse ? kActCollapse : kActBuild;
+                if (Rl.collapse && Rl.csrc != kNone) {
+                    const uint32_t cs = Rl.csrc;
+                    cs_head = cs < kSrcSlot ? pick(ch, cs) : pick(gh, cs & 3u);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        cs_b[k] = cs < kSrcSlot ? pick(ca, (cs & 3u) * 4 + k) : pick(ga, (cs & 1u) * 4 + k);
+                }
+            }
         } else {
-            // first matching rule in source order (dispatch.hpp:119-130)
+            // interpreted matcher: one dependent gather per step below the root
             uint32_t stepnode[kMaxRuleSteps];
             int chosen = -1;
             for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
@@ -162,6 +299,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             }
         }
     }
+    if (prof) pc.mark(3, act);
     long long c1 = prof ? clock64() : 0;
     if (prof) pc.t[0] += c1 - c0;
 
@@ -209,31 +347,50 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // ---- apply
     uint32_t npush = 0, push1 = 0, push_mask = 0;
     bool rewrote = false;
+    // Each lane makes at most one round trip to a waiter word: subscribe to
+    // a pending child (Wait) or publish its own nf (Nf, Collapse).  Both are
+    // issued as ONE compare-and-swap after the branches below, so a warp
+    // mixing the three outcomes pays one atomic latency, not three.
+    uint32_t* wword = nullptr;
+    uint32_t wcmp = 0, wval = 0;
     if (act == kActWait) {
         if (wpos != cursor) rec<W>(arena, i)[kWHead] = sym | (wpos << kSymBits);
-        // subscribe to the pending child; a lost race (another subscriber,
-        // or the child turned nf this very sweep) means polling next sweep
-        uint32_t old = atomicCAS(rec<W>(arena, wchild) + kWWaiter, 0u, i);
-        if (old != 0) {
-            npush = 1;
-            push1 = i;
-        }
+        wword = rec<W>(arena, wchild) + kWWaiter;
+        wcmp = 0u;
+        wval = i;
     } else if (act == kActNf) {
         uint32_t* R = rec<W>(arena, i);
         R[kWEpoch] = s;
-        uint32_t w = atomicExch(R + kWWaiter, kWoken);
-        if (w != 0 && w != kWoken) {
-            npush = 1;
-            push1 = w;
-        }
+        wword = R + kWWaiter;
+        wcmp = own_waiter;
+        wval = kWoken;
     } else if (act == kActCollapse) {
         const DRule& Rl = G.rules[rule];
-        uint32_t src = bind[Rl.root_ref];
-        uint32_t* S = rec<W>(arena, src);
-        uint32_t shead = S[kWHead] & kSymMask;
-        uint32_t sar = G.arity[shead];
+        const uint32_t src = bind[Rl.root_ref];
+        const uint32_t* S = rec<W>(arena, src);
+        uint32_t shead, sar;
         uint32_t b[MAXA];
-        load_args<W>(S, sar, b);
+        if (planned && Rl.csrc != kNone) {
+            // the source record was already in registers (a child or a slot)
+            shead = cs_head;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) b[k] = cs_b[k];
+            sar = G.arity[shead];
+#pragma unroll
+            for (int q = 1; q < MAXA / 4; ++q) {
+                if ((uint32_t)(q * 4) < sar) {
+                    const uint4 v = *reinterpret_cast<const uint4*>(S + kWArgs + q * 4);
+                    b[q * 4 + 0] = v.x;
+                    b[q * 4 + 1] = v.y;
+                    b[q * 4 + 2] = v.z;
+                    b[q * 4 + 3] = v.w;
+                }
+            }
+        } else {
+            shead = S[kWHead] & kSymMask;
+            sar = G.arity[shead];
+            load_args<W>(S, sar, b);
+        }
 #pragma unroll
         for (int j = 0; j < MAXA; ++j)
             if ((uint32_t)j >= sar) b[j] = 0;
@@ -246,11 +403,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
         for (int j = 0; j < MAXA; ++j)
             if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
-        uint32_t w = atomicExch(R + kWWaiter, kWoken);
-        if (w != 0 && w != kWoken) {
-            npush = 1;
-            push1 = w;
-        }
+        wword = R + kWWaiter;
+        wcmp = own_waiter;
+        wval = kWoken;
         rewrote = true;
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
@@ -296,6 +451,28 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
         push1 = i;
         rewrote = true;
+    }
+    if (wword) {
+        uint32_t old = atomicCAS(wword, wcmp, wval);
+        if (act == kActWait) {
+            // lost the subscription race (another subscriber, or the child
+            // turned nf this very sweep): poll next sweep
+            if (old != 0) {
+                npush = 1;
+                push1 = i;
+            }
+        } else {
+            // publish nf: swap in kWoken whatever the word holds (only a
+            // parent subscribing this sweep can change it under us)
+            while (old != wcmp) {
+                wcmp = old;
+                old = atomicCAS(wword, wcmp, kWoken);
+            }
+            if (old != 0 && old != kWoken) {
+                npush = 1;
+                push1 = old;
+            }
+        }
     }
     long long c3 = prof ? clock64() : 0;
     if (prof) pc.t[2] += c3 - c2;
@@ -365,9 +542,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     return __popc(__ballot_sync(0xffffffffu, rewrote));
 }
 
-// All warps of CTAs [block_rank, nblocks) process the frontier in 32-entry
-// chunks; returns this thread's share of the rewrite count (lane 0 of each
-// warp holds its warp's count).
+// All warps of CTAs [block_rank, nblocks) process the frontier in q-entry
+// chunks (chunk_lanes); returns this thread's share of the rewrite count
+// (lane 0 of each warp holds its warp's count).
 template <int W, bool kRich>
 __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const Prog& G, uint32_t* arena,
                                                           const StepCtx& C, const Frontier& F,
@@ -375,10 +552,11 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
                                                           uint32_t nblocks, Slab& slab, bool prof, PhaseClock& pc) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = nblocks * kWarps;
+    const uint32_t q = chunk_lanes(F.M, nblocks);
     unsigned long long rw = 0;
-    for (uint32_t k = block_rank * kWarps + warp; k * 32 < F.M; k += gw) {
-        const uint32_t v = k * 32 + lane;
-        const bool valid = v < F.M;
+    for (uint32_t k = block_rank * kWarps + warp; k * q < F.M; k += gw) {
+        const uint32_t v = k * q + lane;
+        const bool valid = lane < q && v < F.M;
         const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * (kRich ? W : 1) : in;
         rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && warp == 0, pc);
     }
@@ -546,7 +724,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
     const uint32_t lane = threadIdx.x & 31;
     uint32_t* arena = P.arena[L.arena];
     PhaseClock pc;
-    const bool prof = P.profile && lane == 0;
+    const bool prof = kProfBuild && P.profile == 1 && lane == 0;
     for (;;) {
         const uint32_t sc = ss.sc;
         const uint32_t m = ss.count[sc];
@@ -574,10 +752,11 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         if (lane == 0) {
             ss.sc = sc ^ 1;
             record(P, s, width, L, m, 2, global_ns() - t0);
-            if (P.profile) {
+            if (prof) {
                 for (int k = 0; k < 4; ++k) P.ctl->prof[k] += pc.t[k];
                 P.ctl->prof[4] += clock64() - cs;
                 P.ctl->prof[5] += 1;
+                P.ctl->prof[6] += pc.steps;
                 pc = PhaseClock{};
             }
         }
@@ -629,7 +808,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         just_collected = false;
         const uint32_t s = L.sweep + 1;
         const uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
-        const long long cs = (P.profile && threadIdx.x == 0) ? clock64() : 0;
+        const bool profc = kProfBuild && P.profile == 1 && threadIdx.x == 0;
+        const long long cs = profc ? clock64() : 0;
         __syncthreads();  // everyone has read ss.count[sc]
         if (threadIdx.x == 0) {
             ss.count[sc ^ 1] = 0;
@@ -642,7 +822,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
         PhaseClock pc;
         unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
-                                                      P.profile && threadIdx.x == 0, pc);
+                                                      profc, pc);
         const unsigned long long width = block_sum64(rw, sm);
         L.bump += ss.claim;
         L.peak_bump = max(L.peak_bump, L.bump);
@@ -653,10 +833,12 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         if (threadIdx.x == 0) {
             ss.sc = sc ^ 1;
             record(P, s, width, L, m, 1, global_ns() - t0);
-            if (P.profile) {
+            if (profc) {
                 for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
                 ctl->prof[4] += clock64() - cs;
                 ctl->prof[5] += 1;
+                ctl->prof[6] += pc.steps;
+                for (int k = 0; k < 4; ++k) ctl->prof[8 + k] += pc.sub[k];
             }
         }
         __syncthreads();
@@ -798,19 +980,20 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
 
         // ---- grid-wide sweep
         const uint64_t t0 = leader ? global_ns() : 0;
-        const long long cs = (P.profile && leader) ? clock64() : 0;
+        const bool profsw = kProfBuild && P.profile && (P.profile == 1 || m <= P.profile);
+        const long long cs = (profsw && leader) ? clock64() : 0;
         if (threadIdx.x == 0) s_push = 0;
         __syncthreads();
-        const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks);
+        const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks, chunk_lanes(m, nblocks));
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
         StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr};
         PhaseClock pc;
         unsigned long long rw =
             P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                          P.profile && leader, pc)
+                                          profsw && leader, pc)
                    : cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                           P.profile && leader, pc);
+                                           profsw && leader, pc);
         rw = block_sum64(rw, sm);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
@@ -830,10 +1013,12 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         L.sweep = s;
         if (leader) {
             record(P, s, width, L, m, 0, global_ns() - t0);
-            if (P.profile) {
+            if (profsw) {
                 for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
                 ctl->prof[4] += clock64() - cs;
                 ctl->prof[5] += 1;
+                ctl->prof[6] += pc.steps;
+                for (int k = 0; k < 4; ++k) ctl->prof[8 + k] += pc.sub[k];
             }
         }
         if (__ldcg(&ctl->abort_capacity)) {

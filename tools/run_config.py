@@ -11,6 +11,9 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+if "--profile" in " ".join(sys.argv):
+    os.environ.setdefault("TRS_B200_PROFILE_BUILD", "1")  # phase counters live in the profiling build
+
 import numpy as np  # noqa: E402
 
 from paper_2009_07174_b200 import api  # noqa: E402
@@ -45,7 +48,8 @@ def main():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--max-blocks", type=int, default=0)
-    ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--profile", type=int, nargs="?", const=1, default=0,
+                    help="phase cycle accounting; N>1: only grid sweeps of <= N entries")
     args = ap.parse_args()
     texts = texts_for(args.name)
     t0 = time.time()
@@ -56,7 +60,7 @@ def main():
     opts = api.make_options(disable_small=int(args.disable_small), small_enter=args.small_enter,
                             small_exit=args.small_exit, gc_interval=args.gc_interval, variant=args.variant,
                             blocks_per_sm=args.blocks_per_sm, max_blocks=args.max_blocks,
-                            profile=int(args.profile))
+                            profile=args.profile)
     for rep in range(args.reps):
         res = eng.normalize(systems[0], store, opts, words=(rep == args.reps - 1))
         st = res.stats
@@ -72,8 +76,11 @@ def main():
     if args.profile:
         pc = eng.profile_counters()
         n = max(1, pc["sweeps"])
+        ns = max(1, pc["steps"])
         print(json.dumps({"cycles_per_sweep": {k: pc[k] / n for k in ("match", "claim", "apply", "push", "sweep")},
-                          "profiled_sweeps": pc["sweeps"]}), flush=True)
+                          "cycles_per_warp_step": {k: round(pc[k] / ns) for k in ("match", "claim", "apply", "push", "m_record",
+                                                                                  "m_children", "m_slots", "m_rules")},
+                          "profiled_sweeps": pc["sweeps"], "warp_steps": pc["steps"]}), flush=True)
     if args.trace_out:
         np.save(args.trace_out, res.trace)
     if args.ref:
