@@ -43,7 +43,7 @@ struct Ctl {
     unsigned long long max_width;
     unsigned long long gc_ns;
     uint32_t peak_bump;
-    uint32_t pad0;
+    uint32_t sweep0;          // sweeps completed before this run (epochs keep counting)
     // allocator: slots [0, bump) are handed out (in per-warp slabs)
     uint32_t bump;
     // grid barrier: monotonic arrival counter, zeroed by the host per launch
@@ -79,7 +79,6 @@ struct Params {
     uint32_t allow_gc;
     uint32_t fixed_capacity;
     uint32_t max_new;
-    uint32_t sweep0;        // sweeps completed before this run (epochs keep counting)
     uint32_t compact_only;  // >0: run at most this many compaction rounds and exit
     uint32_t prefer_grow;   // out of headroom: grow (host) rather than collect
     uint32_t profile;       // phase cycle accounting of CTA 0 (debug): 1 every sweep, >1 grid sweeps of <= profile entries
@@ -185,6 +184,17 @@ __device__ __forceinline__ unsigned long long block_sum64(unsigned long long v, 
     for (int w = 0; w < kWarps; ++w) t += sm.red[w];
     __syncthreads();
     return t;
+}
+
+// Refcount update, aggregated over the lanes of the warp that hit the same
+// slot in the same instruction (rc_add / rc_sub, sweep_engine.cpp:267-275).
+// A bound variable shared by a whole level of a tree (transform's and
+// build+sum's `n` under Expand/Build) is otherwise one same-address atomic
+// per redex, serialised in its L2 slice; aggregation issues one per warp.
+__device__ __forceinline__ void rc_update(uint32_t* rc, int delta) {
+    const uint32_t act = __activemask();
+    const uint32_t peers = __match_any_sync(act, reinterpret_cast<unsigned long long>(rc));
+    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(rc, (uint32_t)(delta * __popc(peers)));
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {

@@ -164,6 +164,27 @@ __global__ void __launch_bounds__(512) gather_probe_kernel(const uint32_t* __res
     if (acc == 0x9e3779b9u) sink[0] = acc;
 }
 
+// Start of a run (begin = 1) or of a relaunch within one (begin = 0): the
+// host never reads the control block before launching, so a run costs one
+// host synchronisation (the status read-back at the end).
+__global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t begin) {
+    if (threadIdx.x == 0) {
+        if (begin) {
+            c->sweep0 = c->sweep;
+            c->total_rewrites = 0;
+            c->max_width = 0;
+            c->gc_runs = 0;
+            c->small_sweeps = 0;
+            c->gc_ns = 0;
+            c->abort_capacity = 0;
+            c->last_gc_sweep = c->sweep;
+        }
+        c->status = kRunning;
+        c->bar_arrive = 0;
+    }
+    if (threadIdx.x < 8) claim_ctrs[threadIdx.x] = 0;
+}
+
 __global__ void fill_random(uint32_t* idx, uint32_t n, uint64_t seed) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t z = seed + 0x9e3779b97f4a7c15ull * (k + 1);
@@ -209,6 +230,7 @@ struct trs_gpu_engine {
     unsigned long long* d_region_rew = nullptr;  // [2][kMaxGrid]
     uint32_t num_roots = 0;
     Ctl* d_ctl = nullptr;
+    Ctl* h_ctl = nullptr;                 // pinned read-back of the control block
     trs_gpu_sweep_record* d_trace = nullptr;
     uint32_t trace_cap = 0;
     bool loaded = false;
@@ -884,6 +906,7 @@ void trs_gpu_close(trs_gpu_engine* e) {
     cudaSetDevice(e->device);
     free_store(e);
     cudaFree(e->d_prog);
+    if (e->h_ctl) cudaFreeHost(e->h_ctl);
     if (e->load_a) cudaEventDestroy(e->load_a);
     if (e->load_b) cudaEventDestroy(e->load_b);
     cudaStreamDestroy(e->stream);
@@ -935,7 +958,8 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     if (!e) return TRS_GPU_INVALID;
     if (!e->loaded) return fail(e, TRS_GPU_INVALID, "no store loaded");
     cudaSetDevice(e->device);
-    if (int r = drain(e)) return r;
+    // no drain: everything below is ordered on the engine stream
+
     trs_gpu_options opt{};
     if (opt_in) opt = *opt_in;
     e->last_error.clear();
@@ -951,22 +975,9 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     cudaEventCreate(&b);
     int result = TRS_GPU_OK;
     float total_ms = 0.f;
-    uint32_t sweep0 = 0;
-    {
-        Ctl c0;
-        CUDA_TRY(e, cudaMemcpy(&c0, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
-        sweep0 = c0.sweep;
-        c0.total_rewrites = 0;
-        c0.max_width = 0;
-        c0.gc_runs = 0;
-        c0.small_sweeps = 0;
-        c0.gc_ns = 0;
-        c0.status = kRunning;
-        c0.abort_capacity = 0;
-        c0.last_gc_sweep = c0.sweep;
-        CUDA_TRY(e, cudaMemcpy(e->d_ctl, &c0, sizeof(Ctl), cudaMemcpyHostToDevice));
-    }
-    for (;;) {
+    if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
+    Ctl& c = *e->h_ctl;
+    for (int launch = 0;; ++launch) {
         Params P = make_params(e, blocks);
         P.step_budget = opt.step_budget ? opt.step_budget : 1000000000ull;
         P.small_enter = opt.disable_small ? 0 : (opt.small_enter ? opt.small_enter : kBlock);
@@ -976,21 +987,21 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         P.gc_interval = opt.gc_interval;
         P.allow_gc = opt.disable_gc ? 0 : 1;
         P.fixed_capacity = opt.fixed_capacity;
-        P.sweep0 = sweep0;
         P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
         P.profile = opt.profile;
         void* args[] = {&P};
         cudaEventRecord(a, e->stream);
-        reset_barrier(e);
-        reset_barrier(e);
-    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
+        prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, launch == 0 ? 1u : 0u);
+        cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e),
+                                                      e->stream);
+        if (err == cudaSuccess) err = cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream);
         cudaEventRecord(b, e->stream);
         st.launches++;
         if (err != cudaSuccess) {
             result = fail(e, TRS_GPU_CUDA, std::string("step loop launch: ") + cudaGetErrorString(err));
             break;
         }
-        err = cudaEventSynchronize(b);
+        err = cudaEventSynchronize(b);  // the run's only host synchronisation (per launch)
         if (err != cudaSuccess) {
             result = fail(e, TRS_GPU_CUDA, std::string("step loop: ") + cudaGetErrorString(err));
             break;
@@ -998,11 +1009,6 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         float ms = 0.f;
         cudaEventElapsedTime(&ms, a, b);
         total_ms += ms;
-        Ctl c;
-        if (cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost) != cudaSuccess) {
-            result = fail(e, TRS_GPU_CUDA, "control block copy");
-            break;
-        }
         if (c.status == kDone) break;
         if (c.status == kStepBudget) {
             result = fail(e, TRS_GPU_STEP_BUDGET,
@@ -1023,9 +1029,10 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         }
         if (c.status == kNeedGrow) {
             uint64_t m = 0;
-            frontier_extent(e, c, &m);
+            const Ctl cg = c;
+            frontier_extent(e, cg, &m);
             st.regrows++;
-            int r = grow_store(e, (uint64_t)c.bump + 2 * m * e->max_new + (uint64_t)blocks * kWarps * 256 + (1u << 20));
+            int r = grow_store(e, (uint64_t)cg.bump + 2 * m * e->max_new + (uint64_t)blocks * kWarps * 256 + (1u << 20));
             if (r) { result = r; break; }
             continue;
         }
@@ -1034,11 +1041,9 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     }
     cudaEventDestroy(a);
     cudaEventDestroy(b);
-    Ctl c{};
-    cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost);
     st.total_rewrites = c.total_rewrites;
     st.max_width = c.max_width;
-    st.sweeps = c.sweep - sweep0;
+    st.sweeps = c.sweep - c.sweep0;
     st.gc_runs = c.gc_runs;
     st.small_sweeps = c.small_sweeps;
     st.peak_slots = c.peak_bump;
@@ -1048,7 +1053,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     if (e->load_a && e->load_b && cudaEventElapsedTime(&e->load_ms, e->load_a, e->load_b) == cudaSuccess)
         st.load_ms = e->load_ms;
     cudaGetLastError();
-    e->last_sweeps = c.sweep - sweep0;
+    e->last_sweeps = c.sweep - c.sweep0;
     if (result == TRS_GPU_OK && opt.validate) {
         // refcount ghost invariant (sweep_engine.cpp:335-359): rc of every
         // uncollected slot = references from uncollected slots + root pins
@@ -1101,7 +1106,6 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
     CUDA_TRY(e, cudaMemcpy(&c0, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     const int blocks = grid_blocks(e, 0);
     Params P = make_params(e, blocks);
-    P.sweep0 = c0.sweep;
     P.allow_gc = 1;
     P.compact_only = max_rounds ? max_rounds : 8;
     void* args[] = {&P};

@@ -399,10 +399,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
         for (int j = 0; j < MAXA; ++j)
-            if ((uint32_t)j < sar) atomicAdd(rec<W>(arena, b[j]) + kWRc, 1u);
-#pragma unroll
-        for (int j = 0; j < MAXA; ++j)
-            if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
+            if ((uint32_t)j < sar) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -440,17 +437,21 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             for (int j = 0; j < MAXA; ++j) {
                 if ((uint32_t)j < iar) {
                     uint16_t ref = G.refs[I.first_ref + j];
-                    if (!(ref & kRefNode)) atomicAdd(rec<W>(arena, b[j]) + kWRc, 1u);
+                    if (!(ref & kRefNode)) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
                 }
             }
         }
-#pragma unroll
-        for (int j = 0; j < MAXA; ++j)
-            if ((uint32_t)j < ar) atomicSub(rec<W>(arena, a[j]) + kWRc, 1u);
         push_mask = Rl.push_mask;
         npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
         push1 = i;
         rewrote = true;
+    }
+    // the rewritten root drops its old children (after the additions, as
+    // the reference orders them; sweep_engine.cpp:255-256)
+    if (rewrote) {
+#pragma unroll
+        for (int j = 0; j < MAXA; ++j)
+            if ((uint32_t)j < ar) rc_update(rec<W>(arena, a[j]) + kWRc, -1);
     }
     if (wword) {
         uint32_t old = atomicCAS(wword, wcmp, wval);
@@ -570,6 +571,7 @@ struct Local {
     unsigned long long total, maxw;
     uint32_t gc_runs, small_sweeps, last_gc, peak_bump;
     unsigned long long gc_ns;
+    uint32_t sweep0;  // trace records index sweeps from here
 };
 
 __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
@@ -584,6 +586,7 @@ __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
     L.last_gc = __ldcg(&c->last_gc_sweep);
     L.peak_bump = __ldcg(&c->peak_bump);
     L.gc_ns = __ldcg(&c->gc_ns);
+    L.sweep0 = __ldcg(&c->sweep0);
 }
 
 __device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
@@ -607,7 +610,7 @@ enum Plan : uint32_t { kPlanSweep, kPlanGc, kPlanGrow, kPlanFinish, kPlanTrace }
 __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32_t m, bool just_collected,
                                          uint32_t nwarps) {
     const uint32_t s = L.sweep + 1;
-    if (s - P.sweep0 > P.trace_cap) return kPlanTrace;
+    if (s - L.sweep0 > P.trace_cap) return kPlanTrace;
     if (m == 0) return kPlanFinish;
     // worst case: every frontier slot rewrites with the largest template,
     // plus what slab hand-offs can strand (ensure_headroom, sweep_engine.cpp:290-303)
@@ -629,7 +632,7 @@ __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32
 
 __device__ __forceinline__ void record(const Params& P, uint32_t s, unsigned long long width, const Local& L,
                                        uint32_t m, uint32_t mode, uint64_t ns) {
-    const uint32_t k = s - P.sweep0;
+    const uint32_t k = s - L.sweep0;
     if (k == 0 || k > P.trace_cap) return;
     trs_gpu_sweep_record r;
     r.sweep = k;
