@@ -318,34 +318,51 @@ def main():
     max_ms = tot.item()
     all_rw = rw.item()
     value = all_rw / (max_ms * 1e-3)
-    launches = sum(2 + s["launches"] for s in stats)  # load_records + load_frontier + step loop(s)
+    # load_records + load_frontier + init_ctl, then prep_launch + step loop per launch
+    launches = sum(3 + 2 * s["launches"] for s in stats)
 
-    # ---- e2e: pinned host buffers through the C ABI, D2H of the normal-form store
+    # ---- e2e: pinned host buffers through the C ABI: H2D of the SoA store,
+    # run, and the normal form written back in the reference TermStore layout
+    # (trs_gpu_fetch_store: device compaction + pack + D2H of hss, args,
+    # refcounts, nf and roots)
     h2d = (p_hss.numel() + p_args.numel() + p_rc.numel() + p_roots.numel()) * 4
     d2h_bytes = []
     e2e_ms = []
-    host_out = None
+    out = None
+    ma = int(v["maxarity"])
+    L = api.lib()
+    import ctypes
     for k in range(args.warmup + args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        rc = api.lib().trs_gpu_load(eng._h, v["n"], p_roots.data_ptr(), len(roots), p_hss.data_ptr(),
-                                    p_args.data_ptr(), v["maxarity"], p_rc.data_ptr(), 0)
+        rc = L.trs_gpu_load(eng._h, v["n"], p_roots.data_ptr(), len(roots), p_hss.data_ptr(),
+                            p_args.data_ptr(), v["maxarity"], p_rc.data_ptr(), 0)
         assert rc == 0, eng._err()
         s_run = eng.run()
-        s_cmp = eng.compact(8)
-        nbytes, _ = eng.fetch_records()
-        if host_out is None or host_out.numel() < nbytes:
-            host_out = torch.empty(max(nbytes, 1 << 20) * 2, dtype=torch.uint8).pin_memory()
-        eng.fetch_records(host_out.data_ptr(), host_out.numel())
+        n_out = ctypes.c_uint32(0)
+        rc = L.trs_gpu_fetch_store(eng._h, ctypes.byref(n_out), None, None, None, None, None, 0)
+        assert rc == 0, eng._err()
+        N = n_out.value
+        if out is None or out["hss"].numel() < N:
+            cap = int(N * 1.25) + 1024
+            out = {"hss": torch.empty(cap, dtype=torch.int32).pin_memory(),
+                   "args": torch.empty(max(1, ma * cap), dtype=torch.int32).pin_memory(),
+                   "rc": torch.empty(cap, dtype=torch.int32).pin_memory(),
+                   "nf": torch.empty(cap, dtype=torch.uint8).pin_memory(),
+                   "roots": torch.empty(len(roots), dtype=torch.int32).pin_memory()}
+        rc = L.trs_gpu_fetch_store(eng._h, ctypes.byref(n_out), out["roots"].data_ptr(), out["hss"].data_ptr(),
+                                   out["args"].data_ptr() if ma else None, out["rc"].data_ptr(),
+                                   out["nf"].data_ptr(), out["hss"].numel())
+        assert rc == 0, eng._err()
         e1.record(stream)
         e1.synchronize()
         if k >= args.warmup:
             e2e_ms.append(e0.elapsed_time(e1))
-            d2h_bytes.append(nbytes)
-            launches_e2e = 2 + s_run["launches"] + s_cmp["launches"]
+            d2h_bytes.append(N * (4 + 4 * ma + 4 + 1) + 4 * len(roots))
+            launches_e2e = 3 + 2 * s_run["launches"] + 2  # load (3), prep + step loop(s), compaction, pack
     e2e_tot = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
     if world > 1:
         torch.distributed.all_reduce(e2e_tot, op=torch.distributed.ReduceOp.MAX)
@@ -408,8 +425,9 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "rewrites/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(statistics.mean(d2h_bytes)),
-                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_compact + trs_gpu_fetch_records "
-                        "(pinned host), CUDA events on the engine stream", "ms_per_step": statistics.mean(e2e_ms),
+                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_fetch_store (device compaction, "
+                        "pack, D2H of the reference TermStore columns into pinned host memory), CUDA events on "
+                        "the engine stream", "ms_per_step": statistics.mean(e2e_ms),
                 "gpu_launches_per_step": launches_e2e},
         "gpu_launches": launches,
         "clocks": clocks.summary(),

@@ -212,9 +212,13 @@ int trs_gpu_fetch_store(trs_gpu_engine* engine, uint32_t* n, uint32_t* roots, ui
  * callers that bracket calls with their own CUDA events. */
 void* trs_gpu_stream(trs_gpu_engine* engine);
 
-/* Debug phase counters of the last runs (cycles summed over sweeps of CTA
- * 0's thread 0): match, claim, apply, push, whole single-CTA sweep, sweeps. */
-int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out12);
+/* Debug phase counters, accumulated over runs; filled only by the profiling
+ * build (libtrs_b200_prof.so), zeros otherwise.  out18: cycles of the
+ * profiled warp in match, claim, apply, push, whole sweep; sweeps; warp
+ * steps; spare; match sub-phases record, children, slots, rules; then the
+ * collector's phase ns (claim, count, scatter, remap), cascade hops and the
+ * longest cascade. */
+int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out18);
 
 /* Fixed per-sweep overhead probe on the loaded store: `iters` grid barriers
  * (mode 0) or barriers plus the frontier-table staging of a grid sweep

@@ -9,6 +9,10 @@
 #include "device_program.hpp"
 #include "trs_gpu.h"
 
+#ifndef TRS_B200_PROFILE
+#define TRS_B200_PROFILE 0
+#endif
+
 namespace trs_b200 {
 
 constexpr int kBlock = 512;
@@ -51,10 +55,16 @@ struct Ctl {
     // frontier layout: list buffer b holds nregions[b] regions whose
     // (offset, count) pairs live in Params::regions
     uint32_t nregions[2];
+    // a collection left a refcount cascade unfinished (hop cap): garbage remains
+    uint32_t gc_truncated;
+    uint32_t pad1;
     // phase cycle accounting (Params::profile): match, claim, apply, push,
     // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
     // the match sub-phases: record, children, slots, rules
     unsigned long long prof[12];
+    // profiling build: collection phase ns (claim, count, scatter, remap),
+    // cascade hops, longest cascade
+    unsigned long long gcprof[6];
 };
 
 struct Params {

@@ -185,6 +185,32 @@ __global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t begin) {
     if (threadIdx.x < 8) claim_ctrs[threadIdx.x] = 0;
 }
 
+// Device-side write-back in the reference TermStore layout (term_store.hpp:
+// 15-45): hss, column-major args, refcounts and nf of slots [0, n) of a
+// compacted arena, packed into a staging buffer for one D2H per column.
+template <int W>
+__global__ void pack_store(const uint32_t* __restrict__ A, uint32_t n, const uint8_t* __restrict__ arity,
+                           uint32_t ma, uint32_t* __restrict__ hss, uint32_t* __restrict__ args,
+                           uint32_t* __restrict__ rcs, uint8_t* __restrict__ nf) {
+    for (uint32_t y = blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+        if (y == 0) {
+            hss[0] = 0;
+            rcs[0] = 0;
+            nf[0] = 0;
+            for (uint32_t j = 0; j < ma; ++j) args[(size_t)j * n] = 0;
+            continue;
+        }
+        const uint32_t* R = A + (size_t)y * W;
+        const uint4 q0 = *reinterpret_cast<const uint4*>(R);  // head, epoch, rc, waiter
+        const uint32_t sym = q0.x & kSymMask;
+        const uint32_t ar = arity[sym];
+        hss[y] = sym;
+        rcs[y] = q0.z;
+        nf[y] = q0.y != 0;
+        for (uint32_t j = 0; j < ma; ++j) args[(size_t)j * n + y] = j < ar ? R[kWArgs + j] : 0u;
+    }
+}
+
 __global__ void fill_random(uint32_t* idx, uint32_t n, uint64_t seed) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t z = seed + 0x9e3779b97f4a7c15ull * (k + 1);
@@ -231,6 +257,7 @@ struct trs_gpu_engine {
     uint32_t num_roots = 0;
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;                 // pinned read-back of the control block
+    bool dense = false;                   // arena compacted since the last load/run: [1, bump) all live
     trs_gpu_sweep_record* d_trace = nullptr;
     uint32_t trace_cap = 0;
     bool loaded = false;
@@ -826,6 +853,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     e->load_b = b;
     e->num_roots = num_roots;
     e->loaded = true;
+    e->dense = false;
     e->last_sweeps = 0;
     return TRS_GPU_OK;
 }
@@ -959,6 +987,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     if (!e->loaded) return fail(e, TRS_GPU_INVALID, "no store loaded");
     cudaSetDevice(e->device);
     // no drain: everything below is ordered on the engine stream
+    e->dense = false;
 
     trs_gpu_options opt{};
     if (opt_in) opt = *opt_in;
@@ -1088,13 +1117,15 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
 
 void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr; }
 
-int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out12) {
-    if (!e || !e->d_ctl || !out12) return TRS_GPU_INVALID;
+int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out18) {
+    if (!e || !e->d_ctl || !out18) return TRS_GPU_INVALID;
+    uint64_t* out12 = out18;
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     for (int k = 0; k < 12; ++k) out12[k] = c.prof[k];
+    for (int k = 0; k < 6; ++k) out12[12 + k] = c.gcprof[k];
     return TRS_GPU_OK;
 }
 
@@ -1124,6 +1155,7 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
     if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("compaction: ") + cudaGetErrorString(err));
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    e->dense = c.gc_truncated == 0;
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         stats->gc_runs = c.gc_runs - c0.gc_runs;
@@ -1240,39 +1272,42 @@ int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uin
                         uint32_t* refcounts, uint8_t* nf, uint32_t cap) {
     if (!e || !e->loaded || !n) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
-    if (int r = drain(e)) return r;
-    HostArena h;
-    std::vector<uint32_t> roots;
-    int rc = fetch_arena(e, h, roots);
-    if (rc) return rc;
-    // renumber live slots 1..n-1 in arena order
-    std::vector<uint32_t> map(h.base, 0);
-    uint32_t next = 1;
-    for (uint32_t i = 1; i < h.base; ++i)
-        if (h.rec(i)[kWHead] != kDeadHead) map[i] = next++;
-    *n = next;
-    if (!hss) return TRS_GPU_OK;
-    if (cap < next) return fail(e, TRS_GPU_INVALID, "fetch buffer too small");
-    const uint32_t ma = e->max_arity;
-    hss[0] = 0;
-    if (refcounts) refcounts[0] = 0;
-    if (nf) nf[0] = 0;
-    if (args)
-        for (uint32_t j = 0; j < ma; ++j) args[(size_t)j * next] = 0;
-    for (uint32_t i = 1; i < h.base; ++i) {
-        const uint32_t* R = h.rec(i);
-        if (R[kWHead] == kDeadHead) continue;
-        uint32_t k = map[i];
-        uint32_t sym = R[kWHead] & kSymMask;
-        hss[k] = sym;
-        if (refcounts) refcounts[k] = R[kWRc];
-        if (nf) nf[k] = R[kWEpoch] != 0;
-        uint32_t ar = e->arity[sym];
-        if (args)
-            for (uint32_t j = 0; j < ma; ++j) args[(size_t)j * next + k] = j < ar ? map[R[kWArgs + j]] : 0;
+    // garbage is collected on the device first: the copy carries the live
+    // store only, already renumbered 1..n-1 in arena order
+    if (!e->dense) {
+        int r = trs_gpu_compact(e, 8, nullptr);
+        if (r) return r;
     }
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    const uint32_t N = c.bump;
+    *n = N;
+    if (!hss) return TRS_GPU_OK;
+    if (cap < N) return fail(e, TRS_GPU_INVALID, "fetch buffer too small");
+    const uint32_t ma = e->max_arity;
+    // staging in the twin arena (unused between collections): N*(12 + 4*ma) + N bytes <= N*W*4
+    uint8_t* st = reinterpret_cast<uint8_t*>(e->d_arena[c.arena ^ 1]);
+    uint32_t* s_hss = reinterpret_cast<uint32_t*>(st);
+    uint32_t* s_rc = s_hss + N;
+    uint32_t* s_args = s_rc + N;
+    uint8_t* s_nf = reinterpret_cast<uint8_t*>(s_args + (size_t)ma * N);
+    const uint8_t* d_arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
+    const int grid = e->sm_count * 8;
+    switch (e->W) {
+        case 8: pack_store<8><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
+        case 16: pack_store<16><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
+        default: pack_store<32><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
+    }
+    CUDA_TRY(e, cudaGetLastError());
+    CUDA_TRY(e, cudaMemcpyAsync(hss, s_hss, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
+    if (refcounts) CUDA_TRY(e, cudaMemcpyAsync(refcounts, s_rc, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
+    if (args && ma)
+        CUDA_TRY(e, cudaMemcpyAsync(args, s_args, sizeof(uint32_t) * ma * (size_t)N, cudaMemcpyDeviceToHost, e->stream));
+    if (nf) CUDA_TRY(e, cudaMemcpyAsync(nf, s_nf, N, cudaMemcpyDeviceToHost, e->stream));
     if (roots_out)
-        for (uint32_t r = 0; r < roots.size(); ++r) roots_out[r] = map[roots[r]];
+        CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
     return TRS_GPU_OK;
 }
 

@@ -40,21 +40,43 @@ __device__ __forceinline__ uint32_t frontier_phys(const Frontier& f, uint32_t v)
 template <int W>
 __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_t& arena_idx, uint32_t bump,
                                const Frontier& in, uint32_t cur, uint32_t block_rank, uint32_t nblocks,
-                               uint32_t& epoch) {
+                               uint32_t& epoch, bool& truncated, uint32_t max_hops) {
     uint32_t* A = P.arena[arena_idx];
     uint32_t* B = P.arena[arena_idx ^ 1];
     const uint32_t tid = block_rank * kBlock + threadIdx.x;
     const uint32_t nthreads = nblocks * kBlock;
+#if TRS_B200_PROFILE
+    const bool gl = block_rank == 0 && threadIdx.x == 0;
+    uint64_t gt = gl ? global_ns() : 0;
+    unsigned long long hops_total = 0;
+    uint32_t hops_max = 0;
+#define TRS_GC_MARK(k)                                      \
+    if (gl) {                                               \
+        const uint64_t now = global_ns();                   \
+        atomicAdd(&P.ctl->gcprof[k], (unsigned long long)(now - gt)); \
+        gt = now;                                           \
+    }
+#else
+#define TRS_GC_MARK(k)
+#endif
     // phase 1: claim refcount-zero slots and drop their argument references.
-    // A thread follows the cascade it triggers for a bounded number of hops;
-    // the rest waits for a later collection, as the reference defers it.
+    // A thread follows the cascade it triggers for at most max_hops hops (64
+    // inside the step loop, bounding the pause; unbounded for the final
+    // compaction); the rest waits for a later collection, as the reference
+    // defers it.
     for (uint32_t x = 1 + tid; x < bump; x += nthreads) {
         uint32_t* R = rec<W>(A, x);
-        uint32_t head = __ldcg(R + kWHead);
-        if (head == kDeadHead || __ldcg(R + kWRc) != 0) continue;
+        const uint4 hq = __ldcg(reinterpret_cast<const uint4*>(R));  // head, epoch, rc, waiter
+        const uint32_t head = hq.x;
+        if (head == kDeadHead || hq.z != 0) continue;
         if (atomicCAS(R + kWHead, head, kDeadHead) != head) continue;
         uint32_t cur_slot = x, chead = head;
-        for (int hop = 0; hop < 64; ++hop) {
+        for (int hop = 0;; ++hop) {
+            if ((uint32_t)hop == max_hops) {
+                // cascade cut short: the next collection finishes it
+                P.ctl->gc_truncated = 1u;
+                break;
+            }
             uint32_t* C = rec<W>(A, cur_slot);
             uint32_t car = G.arity[chead & kSymMask];
             uint32_t next = 0, nhead = 0;
@@ -68,12 +90,24 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
                     }
                 }
             }
+#if TRS_B200_PROFILE
+            hops_total++;
+            hops_max = max(hops_max, (uint32_t)hop + 1);
+#endif
             if (!next) break;
             cur_slot = next;
             chead = nhead;
         }
     }
+#if TRS_B200_PROFILE
+    atomicAdd(&P.ctl->gcprof[4], hops_total);
+    atomicMax(&P.ctl->gcprof[5], (unsigned long long)hops_max);
+#endif
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_GC_MARK(0)
+    // phase 1 is the flag's only writer; every CTA reads it before the
+    // barriers below, so the clear of the next collection cannot race it
+    truncated = __ldcg(&P.ctl->gc_truncated) != 0;
     // phase 2: live count per CTA range
     const uint32_t span = bump - 1;
     const uint32_t chunk = (span + nblocks - 1) / nblocks;
@@ -85,6 +119,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
     block_scan(cnt, &tot, sm);
     if (threadIdx.x == 0) P.blocksum[block_rank] = tot;
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_GC_MARK(1)
     // phase 3: prefix over CTA sums, then order-preserving scatter into the
     // twin arena with the old -> new map
     uint32_t prefix = 0, all = 0;
@@ -116,6 +151,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
         running += t;
     }
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_GC_MARK(2)
     // phase 4: remap args and waiters, and the frontier into one dense
     // region of the other list buffer, and the roots
     const uint32_t nbump = 1 + all;
@@ -147,6 +183,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
         P.ctl->nregions[cur ^ 1] = 1;
     }
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_GC_MARK(3)
     arena_idx ^= 1;
     return nbump;
 }

@@ -44,9 +44,6 @@ struct StepCtx {
 // Phase cycle accounting is compiled only into the profiling build
 // (libtrs_b200_prof.so, -DTRS_B200_PROFILE=1) so that the production step
 // loop carries none of its registers.
-#ifndef TRS_B200_PROFILE
-#define TRS_B200_PROFILE 0
-#endif
 constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
 
 struct PhaseClock {
@@ -892,11 +889,14 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     Slab slab{0, 0};
     Frontier F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
 
+    bool gc_truncated = false;
     auto collect = [&]() {
         abandon_slab<W>(P.arena[L.arena], slab);
+        if (leader) ctl->gc_truncated = 0u;
         grid_sync(ctl, nblocks, epoch);  // every slab is marked before the collector scans
         const uint64_t t0 = global_ns();
-        L.bump = gc_compact<W>(P, sm, G, L.arena, L.bump, F, L.cur, blockIdx.x, nblocks, epoch);
+        L.bump = gc_compact<W>(P, sm, G, L.arena, L.bump, F, L.cur, blockIdx.x, nblocks, epoch, gc_truncated,
+                               P.compact_only ? 0xFFFFFFFFu : 64u);
         L.cur ^= 1;
         L.gc_runs++;
         L.gc_ns += global_ns() - t0;
@@ -923,7 +923,9 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         for (uint32_t round = 0; round < P.compact_only; ++round) {
             const uint32_t before = L.bump;
             collect();
-            if (L.bump == before) break;
+            // done when every cascade ran to its end (no garbage left) or
+            // a pass reclaimed nothing
+            if (L.bump == before || !gc_truncated) break;
         }
         if (leader) {
             store_local(L, ctl);
