@@ -279,9 +279,23 @@ def main():
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
-    def step_value():
+    def step_value(timed=None):
+        # the whole step is enqueued behind a stream gate before the device
+        # starts it, so host scheduling noise stays outside the event window
+        eng.hold()
+        if timed is not None:
+            timed[0].record(stream)
         eng.load_device(v["n"], roots, d_hss.data_ptr(), d_args.data_ptr(), v["maxarity"], d_rc.data_ptr())
-        return eng.run()
+        eng.run_async()
+        if timed is not None:
+            timed[1].record(stream)
+        eng.release()
+        st = eng.run_wait()
+        if timed is not None and st["launches"] > 1:
+            # a relaunch (arena growth) ran after the closing event: close the
+            # window after it instead (conservative: includes host time)
+            timed[1].record(stream)
+        return st
 
     # ---- warm-up (also sizes the arena once so no growth happens inside timing)
     for _ in range(args.warmup):
@@ -298,12 +312,9 @@ def main():
         for k in range(args.steps):
             with torch.cuda.stream(stream):
                 flush.fill_(k & 0xFF)
-                e0 = torch.cuda.Event(enable_timing=True)
-                e1 = torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-            stats.append(step_value())
-            e1.record(stream)
-            evs.append((e0, e1))
+            ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            stats.append(step_value(ev))
+            evs.append(ev)
         torch.cuda.synchronize()
         if world > 1:
             torch.distributed.barrier()
@@ -328,6 +339,7 @@ def main():
     h2d = (p_hss.numel() + p_args.numel() + p_rc.numel() + p_roots.numel()) * 4
     d2h_bytes = []
     e2e_ms = []
+    e2e_host = []  # host ms of load, run, export, fetch per step (diagnostics)
     out = None
     ma = int(v["maxarity"])
     L = api.lib()
@@ -338,12 +350,16 @@ def main():
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        th0 = time.perf_counter()
         rc = L.trs_gpu_load(eng._h, v["n"], p_roots.data_ptr(), len(roots), p_hss.data_ptr(),
                             p_args.data_ptr(), v["maxarity"], p_rc.data_ptr(), 0)
         assert rc == 0, eng._err()
+        th1 = time.perf_counter()
         s_run = eng.run()
+        th2 = time.perf_counter()
         n_out = ctypes.c_uint32(0)
         rc = L.trs_gpu_fetch_store(eng._h, ctypes.byref(n_out), None, None, None, None, None, 0)
+        th3 = time.perf_counter()
         assert rc == 0, eng._err()
         N = n_out.value
         if out is None or out["hss"].numel() < N:
@@ -357,9 +373,11 @@ def main():
                                    out["args"].data_ptr() if ma else None, out["rc"].data_ptr(),
                                    out["nf"].data_ptr(), out["hss"].numel())
         assert rc == 0, eng._err()
+        th4 = time.perf_counter()
         e1.record(stream)
         e1.synchronize()
         if k >= args.warmup:
+            e2e_host.append([round(1e3 * (b - a), 3) for a, b in ((th0, th1), (th1, th2), (th2, th3), (th3, th4))])
             e2e_ms.append(e0.elapsed_time(e1))
             d2h_bytes.append(N * (4 + 4 * ma + 4 + 1) + 4 * len(roots))
             launches_e2e = 3 + 2 * s_run["launches"] + 2  # load (3), prep + step loop(s), compaction, pack
@@ -425,10 +443,12 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "rewrites/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(statistics.mean(d2h_bytes)),
-                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_fetch_store (device compaction, "
-                        "pack, D2H of the reference TermStore columns into pinned host memory), CUDA events on "
-                        "the engine stream", "ms_per_step": statistics.mean(e2e_ms),
-                "gpu_launches_per_step": launches_e2e},
+                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_fetch_store (device export: "
+                        "mark from the roots, recount references, renumber, pack; D2H of the reference TermStore "
+                        "columns into pinned host memory), CUDA events on the engine stream", "ms_per_step": statistics.mean(e2e_ms),
+                "gpu_launches_per_step": launches_e2e,
+                "step_ms": [round(x, 3) for x in e2e_ms],
+                "host_ms_load_run_export_fetch": e2e_host[-1] if e2e_host else None},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
         "parity": parity,

@@ -190,6 +190,20 @@ int trs_gpu_load_device(trs_gpu_engine* engine, uint32_t n, const uint32_t* root
  * as the failing sweep left it, like the reference. */
 int trs_gpu_run(trs_gpu_engine* engine, const trs_gpu_options* options, trs_gpu_stats* stats);
 
+/* trs_gpu_run split in two: _async enqueues the step loop on the engine
+ * stream and returns at once; _wait blocks until the run ends (relaunching
+ * on the rare arena growth / trace growth) and reports like trs_gpu_run.
+ * One pending run per engine. */
+int trs_gpu_run_async(trs_gpu_engine* engine, const trs_gpu_options* options);
+int trs_gpu_run_wait(trs_gpu_engine* engine, trs_gpu_stats* stats);
+
+/* Stream gate: _hold enqueues a wait on a host-mapped flag so a whole step
+ * (load + run) can be enqueued before the device starts it; _release opens
+ * it.  Nothing that synchronises the engine stream may be called between
+ * the two (e.g. trs_gpu_load, which waits for its copies). */
+int trs_gpu_hold(trs_gpu_engine* engine);
+int trs_gpu_release(trs_gpu_engine* engine);
+
 /* Per-sweep records of the last run; *count receives the number of records
  * (copies min(count, cap)). */
 int trs_gpu_trace(trs_gpu_engine* engine, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count);

@@ -121,6 +121,10 @@ def lib():
         "trs_gpu_load": ([P, U32, P, U32, P, P, U32, P, U64], I),
         "trs_gpu_load_device": ([P, U32, P, U32, P, P, U32, P, U64], I),
         "trs_gpu_run": ([P, ctypes.POINTER(Options), ctypes.POINTER(Stats)], I),
+        "trs_gpu_run_async": ([P, ctypes.POINTER(Options)], I),
+        "trs_gpu_run_wait": ([P, ctypes.POINTER(Stats)], I),
+        "trs_gpu_hold": ([P], I),
+        "trs_gpu_release": ([P], I),
         "trs_gpu_trace": ([P, P, U64, ctypes.POINTER(U64)], I),
         "trs_gpu_canonical": ([P, U32, P, U64, ctypes.POINTER(U64), u32p], I),
         "trs_gpu_fetch_store": ([P, u32p, P, P, P, P, P, U32], I),
@@ -165,7 +169,8 @@ def lib():
 def exported_symbols() -> list[str]:
     return [n for n in ("trs_gpu_device_count", "trs_gpu_open", "trs_gpu_close", "trs_gpu_error_string",
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
-                        "trs_gpu_run", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
+                        "trs_gpu_run", "trs_gpu_run_async", "trs_gpu_run_wait", "trs_gpu_hold",
+                        "trs_gpu_release", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
                         "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
                         "trs_gpu_profile_counters", "trs_gpu_overhead_probe")]
 
@@ -435,6 +440,21 @@ class Engine:
         _raise(rc, self._err())
         return st.as_dict()
 
+    def run_async(self, options: Options | None = None):
+        _raise(lib().trs_gpu_run_async(self._h, ctypes.byref(options or Options())), self._err())
+
+    def run_wait(self) -> dict:
+        st = Stats()
+        rc = lib().trs_gpu_run_wait(self._h, ctypes.byref(st))
+        _raise(rc, self._err())
+        return st.as_dict()
+
+    def hold(self):
+        _raise(lib().trs_gpu_hold(self._h), self._err())
+
+    def release(self):
+        _raise(lib().trs_gpu_release(self._h), self._err())
+
     @property
     def stream(self) -> int:
         """cudaStream_t of this engine (for torch.cuda.ExternalStream + events)."""
@@ -482,19 +502,24 @@ class Engine:
         _raise(rc, self._err())
         return res[0]
 
-    def fetch_store(self) -> dict:
+    def fetch_store(self, maxarity: int, num_roots: int) -> dict:
+        """The live store in the reference TermStore layout (trs_gpu_fetch_store):
+        slots renumbered 1..n-1, args column-major [maxarity, n], refcounts
+        recounted over the exported store, renumbered roots."""
         L = lib()
         n = ctypes.c_uint32(0)
         rc = L.trs_gpu_fetch_store(self._h, ctypes.byref(n), None, None, None, None, None, 0)
         _raise(rc, self._err())
         N = n.value
-        return_roots = np.zeros(1024, np.uint32)
+        roots = np.zeros(max(1, num_roots), np.uint32)
         hss = np.zeros(N, np.uint32)
+        args = np.zeros((maxarity, N), np.uint32)
         rcs = np.zeros(N, np.uint32)
         nf = np.zeros(N, np.uint8)
-        return {"n": N, "hss": hss, "refcounts": rcs, "nf": nf, "_roots": return_roots,
-                "rc": L.trs_gpu_fetch_store(self._h, ctypes.byref(n), return_roots.ctypes.data, hss.ctypes.data,
-                                            None, rcs.ctypes.data, nf.ctypes.data, N)}
+        rc = L.trs_gpu_fetch_store(self._h, ctypes.byref(n), roots.ctypes.data, hss.ctypes.data,
+                                   args.ctypes.data if maxarity else None, rcs.ctypes.data, nf.ctypes.data, N)
+        _raise(rc, self._err())
+        return {"n": N, "hss": hss, "args": args, "refcounts": rcs, "nf": nf, "roots": roots[:num_roots]}
 
     def normalize(self, system: System, store: Store, options: Options | None = None,
                   words: bool = True) -> RunResult:

@@ -57,7 +57,7 @@ struct Ctl {
     uint32_t nregions[2];
     // a collection left a refcount cascade unfinished (hop cap): garbage remains
     uint32_t gc_truncated;
-    uint32_t pad1;
+    uint32_t export_n;        // slots of the last export (export.cuh)
     // phase cycle accounting (Params::profile): match, claim, apply, push,
     // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
     // the match sub-phases: record, children, slots, rules

@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -42,6 +43,7 @@
 
 #include "device_program.hpp"
 #include "sweep.cuh"
+#include "export.cuh"
 #include "trs_gpu.h"
 
 using namespace trs_b200;
@@ -225,6 +227,15 @@ __global__ void fill_random(uint32_t* idx, uint32_t n, uint64_t seed) {
 // ===========================================================================
 // host side
 
+struct RunState {
+    trs_gpu_options opt{};
+    int blocks = 0;
+    uint32_t launches = 0;
+    float total_ms = 0.f;
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool active = false;
+};
+
 struct trs_gpu_engine {
     int device = 0;
     int sm_count = 0;
@@ -257,7 +268,14 @@ struct trs_gpu_engine {
     uint32_t num_roots = 0;
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;                 // pinned read-back of the control block
-    bool dense = false;                   // arena compacted since the last load/run: [1, bump) all live
+    Ctl export_ctl{};                     // control block of the exported state
+    RunState run{};                       // the pending run (trs_gpu_run_async .. trs_gpu_run_wait)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
+    volatile uint32_t* h_gate = nullptr;  // trs_gpu_hold / trs_gpu_release
+    uint32_t* d_gate = nullptr;
+    uint32_t* d_roots_out = nullptr;      // renumbered roots of the export
+    uint32_t roots_out_cap = 0;
+    bool exported = false;                // staging holds the export of the current state
     trs_gpu_sweep_record* d_trace = nullptr;
     uint32_t trace_cap = 0;
     bool loaded = false;
@@ -853,7 +871,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     e->load_b = b;
     e->num_roots = num_roots;
     e->loaded = true;
-    e->dense = false;
+    e->exported = false;
     e->last_sweeps = 0;
     return TRS_GPU_OK;
 }
@@ -935,6 +953,10 @@ void trs_gpu_close(trs_gpu_engine* e) {
     free_store(e);
     cudaFree(e->d_prog);
     if (e->h_ctl) cudaFreeHost(e->h_ctl);
+    if (e->h_gate) cudaFreeHost((void*)e->h_gate);
+    if (e->ev_a) cudaEventDestroy(e->ev_a);
+    if (e->ev_b) cudaEventDestroy(e->ev_b);
+    cudaFree(e->d_roots_out);
     if (e->load_a) cudaEventDestroy(e->load_a);
     if (e->load_b) cudaEventDestroy(e->load_b);
     cudaStreamDestroy(e->stream);
@@ -982,66 +1004,93 @@ int trs_gpu_load_device(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, ui
     return load_impl(e, n, roots, num_roots, d_hss, d_args, max_arity, d_refcounts, capacity);
 }
 
-int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats* stats) {
+}  // extern "C"
+
+namespace {
+
+// One step-loop launch of the pending run on the engine stream: prep, the
+// cooperative launch, the status read-back into pinned memory, the timing
+// events.  Nothing here waits.
+int enqueue_launch(trs_gpu_engine* e) {
+    RunState& R = e->run;
+    const trs_gpu_options& opt = R.opt;
+    Params P = make_params(e, R.blocks);
+    P.step_budget = opt.step_budget ? opt.step_budget : 1000000000ull;
+    P.small_enter = opt.disable_small ? 0 : (opt.small_enter ? opt.small_enter : kBlock);
+    P.small_exit = opt.disable_small ? 0 : (opt.small_exit ? opt.small_exit : 2 * kBlock);
+    if (P.small_exit < P.small_enter) P.small_exit = P.small_enter;
+    P.warp_mode = opt.disable_warp_mode ? 0 : 1;
+    P.gc_interval = opt.gc_interval;
+    P.allow_gc = opt.disable_gc ? 0 : 1;
+    P.fixed_capacity = opt.fixed_capacity;
+    P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
+    P.profile = opt.profile;
+    void* args[] = {&P};
+    cudaEventRecord(R.a, e->stream);
+    prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);
+    cudaError_t err =
+        cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), R.blocks, kBlock, args, dyn_smem(e), e->stream);
+    if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_ctl, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream);
+    cudaEventRecord(R.b, e->stream);
+    R.launches++;
+    if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("step loop launch: ") + cudaGetErrorString(err));
+    return TRS_GPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     if (!e) return TRS_GPU_INVALID;
     if (!e->loaded) return fail(e, TRS_GPU_INVALID, "no store loaded");
+    if (e->run.active) return fail(e, TRS_GPU_INVALID, "a run is already pending (trs_gpu_run_wait)");
     cudaSetDevice(e->device);
     // no drain: everything below is ordered on the engine stream
-    e->dense = false;
-
-    trs_gpu_options opt{};
-    if (opt_in) opt = *opt_in;
+    e->exported = false;
     e->last_error.clear();
-    e->minb = opt.variant == 2 ? 2 : 1;
-    int blocks = grid_blocks(e, opt.blocks_per_sm);
-    if (opt.max_blocks && (int)opt.max_blocks < blocks) blocks = (int)opt.max_blocks;
+    RunState& R = e->run;
+    R = RunState{};
+    if (opt_in) R.opt = *opt_in;
+    e->minb = R.opt.variant == 2 ? 2 : 1;
+    R.blocks = grid_blocks(e, R.opt.blocks_per_sm);
+    if (R.opt.max_blocks && (int)R.opt.max_blocks < R.blocks) R.blocks = (int)R.opt.max_blocks;
+    if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
+    if (!e->ev_a) CUDA_TRY(e, cudaEventCreate(&e->ev_a));
+    if (!e->ev_b) CUDA_TRY(e, cudaEventCreate(&e->ev_b));
+    R.a = e->ev_a;
+    R.b = e->ev_b;
+    R.active = true;
+    int r = enqueue_launch(e);
+    if (r) R.active = false;
+    return r;
+}
+
+int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
+    if (!e) return TRS_GPU_INVALID;
+    RunState& R = e->run;
+    if (!R.active) return fail(e, TRS_GPU_INVALID, "no run pending");
+    cudaSetDevice(e->device);
+    const trs_gpu_options opt = R.opt;
     trs_gpu_stats st{};
-    st.grid_blocks = blocks;
+    st.grid_blocks = R.blocks;
     st.block_threads = kBlock;
     st.record_words = e->W;
-    cudaEvent_t a, b;
-    cudaEventCreate(&a);
-    cudaEventCreate(&b);
     int result = TRS_GPU_OK;
-    float total_ms = 0.f;
-    if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
-    Ctl& c = *e->h_ctl;
-    for (int launch = 0;; ++launch) {
-        Params P = make_params(e, blocks);
-        P.step_budget = opt.step_budget ? opt.step_budget : 1000000000ull;
-        P.small_enter = opt.disable_small ? 0 : (opt.small_enter ? opt.small_enter : kBlock);
-        P.small_exit = opt.disable_small ? 0 : (opt.small_exit ? opt.small_exit : 2 * kBlock);
-        if (P.small_exit < P.small_enter) P.small_exit = P.small_enter;
-        P.warp_mode = opt.disable_warp_mode ? 0 : 1;
-        P.gc_interval = opt.gc_interval;
-        P.allow_gc = opt.disable_gc ? 0 : 1;
-        P.fixed_capacity = opt.fixed_capacity;
-        P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
-        P.profile = opt.profile;
-        void* args[] = {&P};
-        cudaEventRecord(a, e->stream);
-        prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, launch == 0 ? 1u : 0u);
-        cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e),
-                                                      e->stream);
-        if (err == cudaSuccess) err = cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream);
-        cudaEventRecord(b, e->stream);
-        st.launches++;
-        if (err != cudaSuccess) {
-            result = fail(e, TRS_GPU_CUDA, std::string("step loop launch: ") + cudaGetErrorString(err));
-            break;
-        }
-        err = cudaEventSynchronize(b);  // the run's only host synchronisation (per launch)
+    const Ctl& c = *e->h_ctl;
+    for (;;) {
+        cudaError_t err = cudaEventSynchronize(R.b);  // the run's only host synchronisation (per launch)
         if (err != cudaSuccess) {
             result = fail(e, TRS_GPU_CUDA, std::string("step loop: ") + cudaGetErrorString(err));
             break;
         }
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, a, b);
-        total_ms += ms;
+        cudaEventElapsedTime(&ms, R.a, R.b);
+        R.total_ms += ms;
         if (c.status == kDone) break;
         if (c.status == kStepBudget) {
             result = fail(e, TRS_GPU_STEP_BUDGET,
-                          "step budget of " + std::to_string(P.step_budget) +
+                          "step budget of " + std::to_string(opt.step_budget ? opt.step_budget : 1000000000ull) +
                               " rewrites exceeded; the derivation may not terminate");
             break;
         }
@@ -1053,6 +1102,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
         }
         if (c.status == kNeedTrace) {
             int r = grow_trace(e);
+            if (!r) r = enqueue_launch(e);
             if (r) { result = r; break; }
             continue;
         }
@@ -1061,15 +1111,16 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
             const Ctl cg = c;
             frontier_extent(e, cg, &m);
             st.regrows++;
-            int r = grow_store(e, (uint64_t)cg.bump + 2 * m * e->max_new + (uint64_t)blocks * kWarps * 256 + (1u << 20));
+            int r = grow_store(e, (uint64_t)cg.bump + 2 * m * e->max_new + (uint64_t)R.blocks * kWarps * 256 + (1u << 20));
+            if (!r) r = enqueue_launch(e);
             if (r) { result = r; break; }
             continue;
         }
         result = fail(e, TRS_GPU_CUDA, "step loop ended in an unknown state");
         break;
     }
-    cudaEventDestroy(a);
-    cudaEventDestroy(b);
+    R.active = false;
+    st.launches = R.launches;
     st.total_rewrites = c.total_rewrites;
     st.max_width = c.max_width;
     st.sweeps = c.sweep - c.sweep0;
@@ -1077,7 +1128,7 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     st.small_sweeps = c.small_sweeps;
     st.peak_slots = c.peak_bump;
     st.live_terms = c.bump - 1;
-    st.kernel_ms = total_ms;
+    st.kernel_ms = R.total_ms;
     st.gc_ms = c.gc_ns * 1e-6;
     if (e->load_a && e->load_b && cudaEventElapsedTime(&e->load_ms, e->load_a, e->load_b) == cudaSuccess)
         st.load_ms = e->load_ms;
@@ -1113,6 +1164,47 @@ int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt_in, trs_gpu_stats*
     }
     if (stats) *stats = st;
     return result;
+}
+
+int trs_gpu_run(trs_gpu_engine* e, const trs_gpu_options* opt, trs_gpu_stats* stats) {
+    int r = trs_gpu_run_async(e, opt);
+    if (r) return r;
+    return trs_gpu_run_wait(e, stats);
+}
+
+// Stream gate: the engine stream spins on a host-mapped word until
+// trs_gpu_release, so a caller can enqueue a whole step before the device
+// starts it (host scheduling noise then stays outside device timings).
+__global__ void gate_kernel(volatile uint32_t* flag) {
+    uint32_t ns = 64;
+    while (*flag == 0u) {
+        __nanosleep(ns);
+        if (ns < 2048) ns <<= 1;
+    }
+}
+
+int trs_gpu_hold(trs_gpu_engine* e) {
+    if (!e) return TRS_GPU_INVALID;
+    cudaSetDevice(e->device);
+    if (!e->h_gate) {
+        void* hp = nullptr;
+        CUDA_TRY(e, cudaHostAlloc(&hp, sizeof(uint32_t), cudaHostAllocMapped));
+        e->h_gate = static_cast<volatile uint32_t*>(hp);
+        CUDA_TRY(e, cudaHostGetDevicePointer(reinterpret_cast<void**>(&e->d_gate), (void*)e->h_gate, 0));
+    }
+    *e->h_gate = 0u;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    gate_kernel<<<1, 1, 0, e->stream>>>(e->d_gate);
+    CUDA_TRY(e, cudaGetLastError());
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_release(trs_gpu_engine* e) {
+    if (!e || !e->h_gate) return TRS_GPU_INVALID;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    *e->h_gate = 1u;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    return TRS_GPU_OK;
 }
 
 void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr; }
@@ -1155,7 +1247,6 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
     if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("compaction: ") + cudaGetErrorString(err));
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
-    e->dense = c.gc_truncated == 0;
     if (stats) {
         std::memset(stats, 0, sizeof(*stats));
         stats->gc_runs = c.gc_runs - c0.gc_runs;
@@ -1268,45 +1359,100 @@ int trs_gpu_canonical(trs_gpu_engine* e, uint32_t root_index, uint32_t* words, u
     return TRS_GPU_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+template <int W>
+const void* export_ptr() {
+    return reinterpret_cast<const void*>(&export_store<W>);
+}
+
+// Staging layout of an export in the twin arena (bump = slots scanned):
+// hss [bump] | rcs [bump] | args [ma * n] | nf [bump] bytes.
+struct ExportStaging {
+    uint32_t* hss;
+    uint32_t* rcs;
+    uint32_t* args;
+    uint8_t* nf;
+};
+
+ExportStaging export_staging(trs_gpu_engine* e, const Ctl& c) {
+    ExportStaging st;
+    st.hss = e->d_arena[c.arena ^ 1];
+    st.rcs = st.hss + c.bump;
+    st.args = st.rcs + c.bump;
+    st.nf = reinterpret_cast<uint8_t*>(st.args + (size_t)e->max_arity * c.bump);
+    return st;
+}
+
+// Mark from the roots, recount references, renumber and pack (export.cuh).
+int run_export(trs_gpu_engine* e, Ctl& c) {
+    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    const void* fn = e->W == 8 ? export_ptr<8>() : e->W == 16 ? export_ptr<16>() : export_ptr<32>();
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
+    const int blocks = std::min<int>(occ * e->sm_count, (int)kMaxGrid);
+    Params P = make_params(e, blocks);
+    ExportArgs X{};
+    uint32_t* scratch = e->d_list[c.cur ^ 1];  // the frontier lives in list[c.cur]
+    for (int k = 0; k < 3; ++k) X.queue[k] = scratch + (size_t)k * c.bump;
+    X.map = scratch + (size_t)3 * c.bump;
+    X.newrc = e->d_gcmap;
+    X.counters = e->d_blocksum + kMaxGrid;
+    const ExportStaging st = export_staging(e, c);
+    X.hss = st.hss;
+    X.rcs = st.rcs;
+    X.args = st.args;
+    X.nf = st.nf;
+    X.roots_out = e->d_roots_out;
+    X.ma = e->max_arity;
+    uint32_t bump = c.bump;
+    void* args[] = {&P, &X, &bump};
+    CUDA_TRY(e, cudaMemsetAsync(X.counters, 0, sizeof(uint32_t) * 3, e->stream));
+    CUDA_TRY(e, cudaMemsetAsync(X.queue[0], 0, sizeof(uint32_t) * c.bump, e->stream));
+    reset_barrier(e);
+    CUDA_TRY(e, cudaLaunchCooperativeKernel(fn, blocks, kBlock, args, 0, e->stream));
+    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    e->exported = true;
+    e->export_ctl = c;
+    return TRS_GPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uint32_t* hss, uint32_t* args,
                         uint32_t* refcounts, uint8_t* nf, uint32_t cap) {
     if (!e || !e->loaded || !n) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
-    // garbage is collected on the device first: the copy carries the live
-    // store only, already renumbered 1..n-1 in arena order
-    if (!e->dense) {
-        int r = trs_gpu_compact(e, 8, nullptr);
-        if (r) return r;
+    if (e->roots_out_cap < e->num_roots) {
+        cudaFree(e->d_roots_out);
+        CUDA_TRY(e, cudaMalloc(&e->d_roots_out, sizeof(uint32_t) * e->num_roots));
+        e->roots_out_cap = e->num_roots;
     }
-    Ctl c;
-    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
-    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
-    const uint32_t N = c.bump;
+    if (!e->exported) {
+        Ctl c;
+        if (int r = run_export(e, c)) return r;
+    }
+    const Ctl& c = e->export_ctl;
+    const uint32_t N = c.export_n;
     *n = N;
     if (!hss) return TRS_GPU_OK;
     if (cap < N) return fail(e, TRS_GPU_INVALID, "fetch buffer too small");
+    const ExportStaging st = export_staging(e, c);
     const uint32_t ma = e->max_arity;
-    // staging in the twin arena (unused between collections): N*(12 + 4*ma) + N bytes <= N*W*4
-    uint8_t* st = reinterpret_cast<uint8_t*>(e->d_arena[c.arena ^ 1]);
-    uint32_t* s_hss = reinterpret_cast<uint32_t*>(st);
-    uint32_t* s_rc = s_hss + N;
-    uint32_t* s_args = s_rc + N;
-    uint8_t* s_nf = reinterpret_cast<uint8_t*>(s_args + (size_t)ma * N);
-    const uint8_t* d_arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
-    const int grid = e->sm_count * 8;
-    switch (e->W) {
-        case 8: pack_store<8><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
-        case 16: pack_store<16><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
-        default: pack_store<32><<<grid, 256, 0, e->stream>>>(e->d_arena[c.arena], N, d_arity, ma, s_hss, s_args, s_rc, s_nf); break;
-    }
-    CUDA_TRY(e, cudaGetLastError());
-    CUDA_TRY(e, cudaMemcpyAsync(hss, s_hss, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
-    if (refcounts) CUDA_TRY(e, cudaMemcpyAsync(refcounts, s_rc, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaMemcpyAsync(hss, st.hss, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
+    if (refcounts) CUDA_TRY(e, cudaMemcpyAsync(refcounts, st.rcs, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
     if (args && ma)
-        CUDA_TRY(e, cudaMemcpyAsync(args, s_args, sizeof(uint32_t) * ma * (size_t)N, cudaMemcpyDeviceToHost, e->stream));
-    if (nf) CUDA_TRY(e, cudaMemcpyAsync(nf, s_nf, N, cudaMemcpyDeviceToHost, e->stream));
+        CUDA_TRY(e, cudaMemcpyAsync(args, st.args, sizeof(uint32_t) * ma * (size_t)N, cudaMemcpyDeviceToHost, e->stream));
+    if (nf) CUDA_TRY(e, cudaMemcpyAsync(nf, st.nf, N, cudaMemcpyDeviceToHost, e->stream));
     if (roots_out)
-        CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost, e->stream));
+        CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots_out, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost,
+                                    e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
     return TRS_GPU_OK;
 }

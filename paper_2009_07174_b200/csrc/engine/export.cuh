@@ -1,0 +1,172 @@
+// Normal-form export: the live store written back in the reference
+// TermStore layout (term_store.hpp:15-45) without collecting garbage.
+//
+// After a run the arena holds the live term graph plus every slot the run
+// discarded; on the batched configs garbage outnumbers live slots ~8:1, and a
+// refcount collection (gc.cuh) pays one random atomic per garbage edge.  The
+// export instead marks what is reachable from the roots -- the live set by
+// definition (extract, term_store.cpp:77-116, follows the same edges) -- and
+// recounts references on the way: rc(y) = edges from live slots + root pins,
+// the reference's refcount invariant over the exported store
+// (sweep_engine.cpp:335-359).  Then live slots are renumbered 1..n-1 in arena
+// order and packed column by column for one D2H each.
+//
+// Marking runs on one work queue: a thread walks a chain of first-time
+// children itself (S^k numerals, list spines) and queues only the other
+// children, and idle threads take queued items as soon as they appear, so
+// the marking time is about the longest path, not depth x chain length.
+//
+// Scratch: newrc in P.gcmap; the queue and the old -> new map in the list
+// buffer the frontier does NOT occupy; output columns in the twin arena.
+// The arena and the frontier are untouched, so a run can resume afterwards.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace trs_b200 {
+
+struct ExportArgs {
+    uint32_t* queue[3];  // queue[0]: [bump] work items, zeroed by the host
+    uint32_t* map;       // [bump]
+    uint32_t* newrc;     // [bump]
+    uint32_t* counters;  // [3] tail, head, pending (zeroed by the host)
+    uint32_t* hss;       // output columns (staging)
+    uint32_t* args;      // [ma * n]
+    uint32_t* rcs;
+    uint8_t* nf;
+    uint32_t* roots_out;
+    uint32_t ma;
+};
+
+template <int W>
+__global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X, uint32_t bump) {
+    __shared__ Smem sm;
+    const uint32_t* A = P.arena[__ldcg(&P.ctl->arena)];
+    const uint8_t* arity = P.prog + reinterpret_cast<const ProgHeader*>(P.prog)->off_arity;  // global copy
+    const uint32_t nblocks = gridDim.x;
+    const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
+    const uint32_t nthreads = nblocks * kBlock;
+    uint32_t epoch = 0;
+    // clear the reference counters
+    for (uint32_t y = tid; y < bump; y += nthreads) X.newrc[y] = 0;
+    grid_sync(P.ctl, nblocks, epoch);
+    // Marking runs on one shared work queue with no levels: an S^k numeral
+    // under a deep tree would otherwise cost a whole chain walk per level.
+    // Items are pushed by a tail counter into zeroed slots; a thread claims
+    // the next slot by a head counter and waits for it to be filled, or for
+    // `pending` (pushed but unfinished items) to reach zero, which means no
+    // further push can happen.  Every root occurrence pins once.
+    uint32_t* tail = X.counters + 0;
+    uint32_t* head = X.counters + 1;
+    uint32_t* pending = X.counters + 2;
+    uint32_t* Q = X.queue[0];
+    for (uint32_t r = tid; r < P.num_roots; r += nthreads) {
+        const uint32_t x = P.roots[r];
+        if (atomicAdd(X.newrc + x, 1u) == 0u) {
+            atomicAdd(pending, 1u);
+            Q[atomicAdd(tail, 1u)] = x;
+        }
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    for (;;) {
+        const uint32_t i = atomicAdd(head, 1u);
+        uint32_t x = 0;
+        uint32_t ns = 32;
+        while ((x = ld_acquire(Q + i)) == 0u) {
+            // pending reaches zero only after every push (release below):
+            // one more look at the slot settles it
+            if (ld_acquire(pending) == 0u) {
+                x = ld_acquire(Q + i);
+                break;
+            }
+            __nanosleep(ns);
+            if (ns < 1024) ns <<= 1;
+        }
+        if (x == 0u) break;
+        while (x) {
+            const uint32_t* R = A + (size_t)x * W;
+            const uint4 h4 = __ldcg(reinterpret_cast<const uint4*>(R));
+            const uint4 a4 = __ldcg(reinterpret_cast<const uint4*>(R + kWArgs));
+            const uint32_t ar = arity[h4.x & kSymMask];
+            uint32_t next = 0;
+            for (uint32_t j = 0; j < ar; ++j) {
+                const uint32_t c = j == 0 ? a4.x : j == 1 ? a4.y : j == 2 ? a4.z : j == 3 ? a4.w : __ldcg(R + kWArgs + j);
+                if (atomicAdd(X.newrc + c, 1u) == 0u) {
+                    if (next == 0) {
+                        next = c;  // keep walking: a chain stays in one thread
+                    } else {
+                        atomicAdd(pending, 1u);
+                        const uint32_t t = atomicAdd(tail, 1u);
+                        asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(Q + t), "r"(c) : "memory");
+                    }
+                }
+            }
+            x = next;
+        }
+        red_release_add(pending, 0xFFFFFFFFu);  // -1, ordered after this item's pushes
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    // renumber live slots in arena order: per-CTA contiguous ranges
+    const uint32_t span = bump - 1;
+    const uint32_t chunk = (span + nblocks - 1) / nblocks;
+    const uint32_t lo = 1 + blockIdx.x * chunk;
+    const uint32_t hi = min(bump, lo + chunk);
+    uint32_t cnt = 0;
+    for (uint32_t y = lo + threadIdx.x; y < hi; y += kBlock) cnt += __ldcg(X.newrc + y) != 0u;
+    uint32_t tot;
+    block_scan(cnt, &tot, sm);
+    if (threadIdx.x == 0) P.blocksum[blockIdx.x] = tot;
+    grid_sync(P.ctl, nblocks, epoch);
+    uint32_t prefix = 0, all = 0;
+    for (uint32_t b = threadIdx.x; b < nblocks; b += kBlock) {
+        const uint32_t c = __ldcg(P.blocksum + b);
+        all += c;
+        if (b < blockIdx.x) prefix += c;
+    }
+    {
+        uint32_t t1, t2;
+        block_scan(prefix, &t1, sm);
+        block_scan(all, &t2, sm);
+        prefix = t1;
+        all = t2;
+    }
+    uint32_t running = 1 + prefix;
+    for (uint32_t y0 = lo; y0 < hi; y0 += kBlock) {
+        const uint32_t y = y0 + threadIdx.x;
+        const bool live = y < hi && __ldcg(X.newrc + y) != 0u;
+        uint32_t t;
+        const uint32_t e = block_scan(live ? 1u : 0u, &t, sm);
+        if (y < hi) X.map[y] = live ? running + e : 0u;
+        running += t;
+    }
+    const uint32_t n = 1 + all;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        P.ctl->export_n = n;
+        X.map[0] = 0;
+    }
+    grid_sync(P.ctl, nblocks, epoch);
+    // pack the columns
+    for (uint32_t y = 1 + tid; y < bump; y += nthreads) {
+        const uint32_t rc = __ldcg(X.newrc + y);
+        if (!rc) continue;
+        const uint32_t k = __ldcg(X.map + y);
+        const uint32_t* R = A + (size_t)y * W;
+        const uint4 q0 = __ldcg(reinterpret_cast<const uint4*>(R));  // head, epoch, rc, waiter
+        const uint32_t sym = q0.x & kSymMask;
+        const uint32_t ar = arity[sym];
+        X.hss[k] = sym;
+        X.rcs[k] = rc;
+        X.nf[k] = q0.y != 0;
+        for (uint32_t j = 0; j < X.ma; ++j)
+            X.args[(size_t)j * n + k] = j < ar ? __ldcg(X.map + __ldcg(R + kWArgs + j)) : 0u;
+    }
+    if (tid == 0) {
+        X.hss[0] = 0;
+        X.rcs[0] = 0;
+        X.nf[0] = 0;
+        for (uint32_t j = 0; j < X.ma; ++j) X.args[(size_t)j * n] = 0;
+    }
+    for (uint32_t r = tid; r < P.num_roots; r += nthreads) X.roots_out[r] = __ldcg(X.map + P.roots[r]);
+}
+
+}  // namespace trs_b200

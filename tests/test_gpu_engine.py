@@ -152,6 +152,46 @@ def test_compact_and_fetch(engine):
     assert g["nodes"] <= c["live_terms"] <= 4 * g["nodes"]
 
 
+@pytest.mark.parametrize("name", ["fibbatch64_s3", "mergesort50_s42", "transform6"])
+def test_fetch_store_export(engine, name):
+    """Device export in the reference TermStore layout: the live store only,
+    refcounts = references from exported slots + root pins (the reference's
+    ghost invariant, sweep_engine.cpp:335-359), every slot reachable, and the
+    canonical words of every root unchanged."""
+    g = CASES[name]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    v = st.view()
+    engine.set_program(s)
+    engine.load(st)
+    engine.run()
+    before = [engine.canonical(k) for k in range(v["num_roots"])]
+    out = engine.fetch_store(v["maxarity"], v["num_roots"])
+    n = out["n"]
+    arity = np.zeros(n, np.int64)
+    counted = np.zeros(n, np.int64)
+    for r in out["roots"]:
+        counted[r] += 1
+    ar_of = [s.symbol_arity(f) for f in range(s.num_symbols)]
+    for y in range(1, n):
+        a = ar_of[out["hss"][y]]
+        arity[y] = a
+        for j in range(a):
+            c = out["args"][j, y]
+            assert 0 < c < n
+            counted[c] += 1
+        for j in range(a, v["maxarity"]):
+            assert out["args"][j, y] == 0
+    np.testing.assert_array_equal(out["refcounts"][1:], counted[1:])
+    assert (counted[1:] > 0).all()  # nothing unreachable survives
+    assert out["nf"][1:].all()      # a normal form
+    # the export leaves the engine state alone
+    after = [engine.canonical(k) for k in range(v["num_roots"])]
+    for a, b in zip(before, after):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(before[0], np.asarray(g["words"], np.uint32))
+
+
 def test_trace_records(engine):
     # sweep_engine_tests.cpp:238-255
     res = run(engine, CASES["mergesort10_s3"]["text"])
