@@ -96,6 +96,7 @@ struct Params {
     uint32_t probe_iters;   // >0: time this many grid barriers and exit (trs_gpu_overhead_probe)
     uint32_t probe_mode;
     uint32_t rich;          // grid frontier entries carry record payloads (W words) instead of bare slots
+    uint32_t debug_flags;   // experiments (trs_gpu_options.reserved[0])
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {
@@ -196,15 +197,23 @@ __device__ __forceinline__ unsigned long long block_sum64(unsigned long long v, 
     return t;
 }
 
-// Refcount update, aggregated over the lanes of the warp that hit the same
-// slot in the same instruction (rc_add / rc_sub, sweep_engine.cpp:267-275).
+// Refcount update (rc_add / rc_sub, sweep_engine.cpp:267-275), aggregated
+// over the lanes of the warp that hit the same slot as the first active lane.
 // A bound variable shared by a whole level of a tree (transform's and
 // build+sum's `n` under Expand/Build) is otherwise one same-address atomic
-// per redex, serialised in its L2 slice; aggregation issues one per warp.
+// per redex, serialised in its L2 slice; this issues one per warp.  The test
+// is a shuffle and a ballot (a full match_any costs more than it saves when
+// slots are distinct, the common case).
 __device__ __forceinline__ void rc_update(uint32_t* rc, int delta) {
     const uint32_t act = __activemask();
-    const uint32_t peers = __match_any_sync(act, reinterpret_cast<unsigned long long>(rc));
-    if ((threadIdx.x & 31) == (uint32_t)(__ffs(peers) - 1)) atomicAdd(rc, (uint32_t)(delta * __popc(peers)));
+    const int first = __ffs(act) - 1;
+    const unsigned long long mine = reinterpret_cast<unsigned long long>(rc);
+    const unsigned long long lead = __shfl_sync(act, mine, first);
+    const uint32_t same = __ballot_sync(act, mine == lead);
+    // one reduction instruction for the warp: the first lane carries its
+    // group's sum, the group's other lanes nothing, everyone else its delta
+    const int v = mine != lead ? delta : (int)(threadIdx.x & 31) == first ? delta * __popc(same) : 0;
+    if (v) atomicAdd(rc, (uint32_t)v);
 }
 
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {

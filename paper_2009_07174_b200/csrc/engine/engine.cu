@@ -1025,6 +1025,7 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.fixed_capacity = opt.fixed_capacity;
     P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
     P.profile = opt.profile;
+    P.debug_flags = opt.reserved[0];
     void* args[] = {&P};
     cudaEventRecord(R.a, e->stream);
     prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("name")
     ap.add_argument("--save", default="")
     ap.add_argument("--variant", type=int, default=0)
+    ap.add_argument("--debug-flags", type=int, default=0)
     args = ap.parse_args()
     texts = texts_for(args.name)
     systems = [api.System(t) for t in texts]
@@ -32,6 +33,7 @@ def main():
     eng = api.Engine(0)
     eng.set_program(systems[0])
     opts = api.make_options(variant=args.variant)
+    opts.reserved[0] = args.debug_flags
     for _ in range(2):
         eng.load(store)
         st = eng.run(opts)
