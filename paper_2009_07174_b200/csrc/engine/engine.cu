@@ -251,6 +251,8 @@ struct trs_gpu_engine {
     std::vector<uint32_t> arity;
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
+    bool resident_on = false;  // this run reserves the shared-memory resident arena
+    uint32_t input_n = 0;      // slots of the loaded store
     uint32_t rich = 0;  // frontier entry format of the loaded store (fixed at load time)
 
     // store
@@ -641,7 +643,21 @@ const void* step_loop_for(int W, int minb) {
     }
 }
 
-size_t dyn_smem(const trs_gpu_engine* e) { return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t); }
+// Dynamic shared memory of the step loop: program blob, the two single-CTA
+// frontier lists, and (when enabled) the resident arena of the single-CTA
+// mode (sweep.cuh, run_small).
+constexpr size_t kSmemBudget = 227 * 1024 - 12 * 1024;  // dynamic bytes, leaving room for static smem
+size_t dyn_base(const trs_gpu_engine* e) { return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t); }
+uint32_t resident_slots(const trs_gpu_engine* e) {
+    const size_t base = dyn_base(e);
+    if (base >= kSmemBudget) return 0;
+    size_t slots = (kSmemBudget - base) / ((size_t)e->W * 4);
+    slots = std::min<size_t>(slots, kSmallCap);  // local_gc keeps its map in an idle frontier list
+    return slots >= 256 ? (uint32_t)slots : 0u;
+}
+size_t dyn_smem(const trs_gpu_engine* e) {
+    return dyn_base(e) + (e->resident_on ? (size_t)resident_slots(e) * e->W * 4 : 0);
+}
 
 int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     size_t rec_bytes = (size_t)e->W * 4;
@@ -870,6 +886,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     e->load_a = a;
     e->load_b = b;
     e->num_roots = num_roots;
+    e->input_n = n;
     e->loaded = true;
     e->exported = false;
     e->last_sweeps = 0;
@@ -1026,6 +1043,8 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
     P.profile = opt.profile;
     P.debug_flags = opt.reserved[0];
+    P.local_cap = e->resident_on ? resident_slots(e) : 0u;
+    P.local_enter = P.local_cap / 2;
     void* args[] = {&P};
     cudaEventRecord(R.a, e->stream);
     prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);
@@ -1054,6 +1073,9 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     R = RunState{};
     if (opt_in) R.opt = *opt_in;
     e->minb = R.opt.variant == 2 ? 2 : 1;
+    // the resident arena costs L1 capacity on every grid sweep: reserve it
+    // only for stores small enough to start resident (single-term runs)
+    e->resident_on = !(R.opt.reserved[1] & 1u) && resident_slots(e) != 0 && e->input_n <= resident_slots(e) / 2;
     R.blocks = grid_blocks(e, R.opt.blocks_per_sm);
     if (R.opt.max_blocks && (int)R.opt.max_blocks < R.blocks) R.blocks = (int)R.opt.max_blocks;
     if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));

@@ -39,6 +39,8 @@ struct StepCtx {
     uint32_t* out;        // output region of the next frontier
     uint32_t* push_ctr;   // entries pushed into `out` (shared memory)
     uint32_t* abort_flag; // shared flag raised with ctl->abort_capacity (may be null)
+    uint64_t cap;         // slots of the arena being swept (global or shared-memory resident)
+    uint32_t slab;        // fresh slots a warp claims at a time (0: exactly what a step needs)
 };
 
 // Phase cycle accounting is compiled only into the profiling build
@@ -308,11 +310,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     if (total) {
         if (slab.end - slab.cur < total) {
             abandon_slab<W>(arena, slab);
-            uint32_t size = max(P.slab, total);
+            uint32_t size = max(C.slab, total);
             uint32_t off = 0;
             if (lane == 0) {
                 off = atomicAdd(C.claim_ctr, size);
-                if ((uint64_t)C.bump + off + size > P.capacity && P.fixed_capacity) {
+                if ((uint64_t)C.bump + off + size > C.cap && P.fixed_capacity) {
                     // a full slab does not fit: take exactly what this step needs
                     size = total;
                     off = atomicAdd(C.claim_ctr, size);
@@ -321,7 +323,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             off = __shfl_sync(0xffffffffu, off, 0);
             size = __shfl_sync(0xffffffffu, size, 0);
             const uint64_t start = (uint64_t)C.bump + off;
-            if (start + size > P.capacity) {
+            if (start + size > C.cap) {
                 // fixed capacity exhausted: the reference raises Capacity (sweep_engine.cpp:221-226)
                 if (lane == 0) {
                     atomicExch(&P.ctl->abort_capacity, 1u);
@@ -717,18 +719,102 @@ struct SmallState {
     Local L;            // hand-over from warp mode to the whole CTA
 };
 
+// Copy records [0, n) between arenas (global <-> shared memory), CTA-wide.
+template <int W>
+__device__ __forceinline__ void copy_records(uint32_t* dst, const uint32_t* src, uint32_t n) {
+    const uint32_t q = n * (W / 4);
+    for (uint32_t k = threadIdx.x; k < q; k += kBlock)
+        reinterpret_cast<uint4*>(dst)[k] = reinterpret_cast<const uint4*>(src)[k];  // generic: either side may be shared
+}
+
+// Collection of a shared-memory resident arena by CTA 0 (the grid-wide
+// gc_compact restated for one CTA): claim refcount-zero slots and follow
+// their cascades to the end, renumber live slots in order (map in the idle
+// frontier list `map`, so the resident arena holds at most kSmallCap
+// slots), move records down chunk by chunk, and remap arguments, waiter
+// words, the frontier `list` and the roots.  Returns the new bump pointer.
+template <int W>
+__device__ uint32_t local_gc(const Params& P, const Prog& G, Smem& sm, uint32_t* A, uint32_t bump, uint32_t* list,
+                             uint32_t m, uint32_t* map) {
+    for (uint32_t x = 1 + threadIdx.x; x < bump; x += kBlock) {
+        uint32_t* R = rec<W>(A, x);
+        const uint32_t head = R[kWHead];
+        if (head == kDeadHead || R[kWRc] != 0) continue;
+        if (atomicCAS(R + kWHead, head, kDeadHead) != head) continue;
+        uint32_t cur_slot = x, chead = head;
+        for (;;) {
+            const uint32_t* C = rec<W>(A, cur_slot);
+            const uint32_t car = G.arity[chead & kSymMask];
+            uint32_t next = 0, nhead = 0;
+            for (uint32_t j = 0; j < car; ++j) {
+                const uint32_t c = C[kWArgs + j];
+                if (atomicSub(rec<W>(A, c) + kWRc, 1u) == 1u && next == 0) {
+                    const uint32_t h = rec<W>(A, c)[kWHead];
+                    if (h != kDeadHead && atomicCAS(rec<W>(A, c) + kWHead, h, kDeadHead) == h) {
+                        next = c;
+                        nhead = h;
+                    }
+                }
+            }
+            if (!next) break;
+            cur_slot = next;
+            chead = nhead;
+        }
+    }
+    __syncthreads();
+    uint32_t running = 1;
+    for (uint32_t x0 = 0; x0 < bump; x0 += kBlock) {
+        const uint32_t x = x0 + threadIdx.x;
+        const bool live = x > 0 && x < bump && rec<W>(A, x)[kWHead] != kDeadHead;
+        uint32_t t;
+        const uint32_t e = block_scan(live ? 1u : 0u, &t, sm);
+        if (x < bump) map[x] = live ? running + e : 0u;
+        running += t;
+    }
+    __syncthreads();
+    // order-preserving move: targets never exceed sources, and every earlier
+    // chunk has landed before this chunk's records are read
+    for (uint32_t x0 = 0; x0 < bump; x0 += kBlock) {
+        const uint32_t x = x0 + threadIdx.x;
+        const uint32_t to = x < bump ? map[x] : 0u;
+        uint4 v[W / 4];
+        if (to) {
+#pragma unroll
+            for (int q = 0; q < W / 4; ++q) v[q] = reinterpret_cast<const uint4*>(rec<W>(A, x))[q];
+        }
+        __syncthreads();
+        if (to) {
+#pragma unroll
+            for (int q = 0; q < W / 4; ++q) reinterpret_cast<uint4*>(rec<W>(A, to))[q] = v[q];
+        }
+        __syncthreads();
+    }
+    for (uint32_t y = 1 + threadIdx.x; y < running; y += kBlock) {
+        uint32_t* R = rec<W>(A, y);
+        const uint32_t car = G.arity[R[kWHead] & kSymMask];
+        for (uint32_t j = 0; j < car; ++j) R[kWArgs + j] = map[R[kWArgs + j]];
+        const uint32_t w = R[kWWaiter];
+        if (w != 0 && w != kWoken) R[kWWaiter] = map[w];
+    }
+    for (uint32_t v = threadIdx.x; v < m; v += kBlock) list[v] = map[list[v]];
+    for (uint32_t r = threadIdx.x; r < P.num_roots; r += kBlock) P.roots[r] = map[__ldcg(P.roots + r)];
+    __syncthreads();
+    return running;
+}
+
 // Warp 0 of CTA 0 runs sweeps alone while the frontier fits one warp.
 template <int W>
 __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, SmallState& ss, Local& L,
-                            bool& just_collected, Slab& slab) {
+                            bool& just_collected, Slab& slab, uint32_t* arena, uint64_t cap, uint32_t slab_size) {
     const uint32_t lane = threadIdx.x & 31;
-    uint32_t* arena = P.arena[L.arena];
     PhaseClock pc;
     const bool prof = kProfBuild && P.profile == 1 && lane == 0;
     for (;;) {
         const uint32_t sc = ss.sc;
         const uint32_t m = ss.count[sc];
         if (m == 0 || m > 32) break;
+        // a resident arena must hold the worst case of this sweep
+        if (slab_size == 0 && (uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap) break;
         if (plan(P, L, m, just_collected, 1) != kPlanSweep) break;
         just_collected = false;
         const uint32_t s = L.sweep + 1;
@@ -739,7 +825,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             ss.claim = 0;
         }
         __syncwarp();
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size};
         const bool valid = lane < m;
         const uint32_t width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
         __syncwarp();
@@ -787,22 +873,62 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     }
     __syncthreads();
     uint32_t* arena = P.arena[L.arena];
+    uint64_t cap = P.capacity;
+    uint32_t slab_size = P.slab;
+    // Resident mode: the whole allocated store fits the CTA's shared memory,
+    // so it moves there (same slot ids) and every gather, claim and atomic of
+    // these sweeps is a shared-memory access; claims are exact (no slabs),
+    // a full resident arena is compacted in place (local_gc), and the store
+    // moves back when the frontier outgrows this mode or stops fitting.
+    uint32_t* const resident_arena = slist + 2 * kSmallCap;
+    bool resident = P.local_cap != 0 && L.bump <= P.local_enter;
+    if (resident) {
+        abandon_slab<W>(arena, slab);
+        __syncthreads();
+        copy_records<W>(resident_arena, arena, L.bump);
+        __syncthreads();
+        arena = resident_arena;
+        cap = min((uint64_t)P.local_cap, P.capacity);  // a fixed capacity binds here too
+        slab_size = 0;
+    }
+    auto leave_resident = [&]() {
+        copy_records<W>(P.arena[L.arena], resident_arena, L.bump);
+        __syncthreads();
+        arena = P.arena[L.arena];
+        cap = P.capacity;
+        slab_size = P.slab;
+        resident = false;
+    };
     const uint32_t warp = threadIdx.x >> 5;
     for (;;) {
         const uint32_t sc = ss.sc;
         const uint32_t m = ss.count[sc];
         if (m > exit_m) break;
+        if (resident && (uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap) {
+            if (P.allow_gc) {
+                const uint64_t t0 = global_ns();
+                L.bump = local_gc<W>(P, G, sm, arena, L.bump, slist + sc * kSmallCap, m, slist + (sc ^ 1) * kSmallCap);
+                L.gc_runs++;
+                L.gc_ns += global_ns() - t0;
+                L.last_gc = L.sweep + 1;
+            }
+            // keep half the resident arena free, else hand back to HBM (where
+            // growth, collection or the fixed-capacity fault take over)
+            if ((uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap / 2) leave_resident();
+        }
         if (plan(P, L, m, just_collected, kWarps) != kPlanSweep) break;
         if (P.warp_mode && m <= 32) {
             if (warp == 0) {
-                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab);
+                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size);
                 if ((threadIdx.x & 31) == 0) ss.L = L;
             }
             __syncthreads();
             L = ss.L;
             just_collected = false;
             if (L.total > P.step_budget || ss.abort) break;
-            if (ss.count[ss.sc] <= 32) break;  // warp mode stopped for another reason (plan / empty)
+            const uint32_t m2 = ss.count[ss.sc];
+            if (m2 <= 32 && !(resident && m2 && (uint64_t)L.bump + (uint64_t)m2 * P.max_new + 1 > cap))
+                break;  // warp mode stopped for another reason (plan / empty)
             continue;
         }
         just_collected = false;
@@ -819,7 +945,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         Frontier Fs{1, m, nullptr, nullptr};
         uint32_t zero_off = 0;
         Fs.off = &zero_off;
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort};
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size};
         PhaseClock pc;
         unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
                                                       profc, pc);
@@ -832,7 +958,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         L.small_sweeps++;
         if (threadIdx.x == 0) {
             ss.sc = sc ^ 1;
-            record(P, s, width, L, m, 1, global_ns() - t0);
+            record(P, s, width, L, m, resident ? 3 : 1, global_ns() - t0);
             if (profc) {
                 for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
                 ctl->prof[4] += clock64() - cs;
@@ -844,6 +970,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         __syncthreads();
         if (L.total > P.step_budget || ss.abort) break;
     }
+    if (resident) leave_resident();
     // hand the frontier back to the grid as one region of the global list
     const uint32_t m = ss.count[ss.sc];
     uint32_t* gout = P.list[L.cur];
@@ -992,7 +1119,8 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks, chunk_lanes(m, nblocks));
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
-        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr};
+        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr,
+                  P.capacity, P.slab};
         PhaseClock pc;
         unsigned long long rw =
             P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,

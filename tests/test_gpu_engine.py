@@ -192,6 +192,25 @@ def test_fetch_store_export(engine, name):
     np.testing.assert_array_equal(before[0], np.asarray(g["words"], np.uint32))
 
 
+@pytest.mark.parametrize("name", ["ackermann23", "fib12", "mergesort50_s42", "reverse64", "unit_two_waiters"])
+@pytest.mark.parametrize("gc_interval", [0, 3])
+def test_resident_mode_is_invisible(engine, name, gc_interval):
+    """The shared-memory resident arena of the single-CTA mode (with its own
+    compactions) gives the same widths, rewrites and normal form as sweeping
+    the store in HBM."""
+    g = CASES[name]
+    outs = []
+    for no_resident in (0, 1):
+        o = api.make_options(gc_interval=gc_interval)
+        o.reserved[1] = no_resident
+        res = api.normalize_texts(g["text"], engine=engine, options=o)
+        outs.append(res)
+        assert res.total_rewrites == g["rewrites"]
+        np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+        np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+    assert outs[0].trace["mode"].max() >= 1
+
+
 def test_trace_records(engine):
     # sweep_engine_tests.cpp:238-255
     res = run(engine, CASES["mergesort10_s3"]["text"])

@@ -48,6 +48,7 @@ def main():
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--trace-out", default="")
     ap.add_argument("--max-blocks", type=int, default=0)
+    ap.add_argument("--no-resident", action="store_true")
     ap.add_argument("--profile", type=int, nargs="?", const=1, default=0,
                     help="phase cycle accounting; N>1: only grid sweeps of <= N entries")
     args = ap.parse_args()
@@ -61,6 +62,7 @@ def main():
                             small_exit=args.small_exit, gc_interval=args.gc_interval, variant=args.variant,
                             blocks_per_sm=args.blocks_per_sm, max_blocks=args.max_blocks,
                             profile=args.profile)
+    opts.reserved[1] = 1 if args.no_resident else 0
     for rep in range(args.reps):
         res = eng.normalize(systems[0], store, opts, words=(rep == args.reps - 1))
         st = res.stats

@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--save", default="")
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--debug-flags", type=int, default=0)
+    ap.add_argument("--no-resident", action="store_true")
     args = ap.parse_args()
     texts = texts_for(args.name)
     systems = [api.System(t) for t in texts]
@@ -34,6 +35,7 @@ def main():
     eng.set_program(systems[0])
     opts = api.make_options(variant=args.variant)
     opts.reserved[0] = args.debug_flags
+    opts.reserved[1] = 1 if args.no_resident else 0
     for _ in range(2):
         eng.load(store)
         st = eng.run(opts)
