@@ -42,6 +42,8 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-GPU table")
     ap.add_argument("--configs-only", action="store_true")
+    ap.add_argument("--no-gate", action="store_true",
+                    help="enqueue steps without the stream gate (needed under ncu, which serialises launches)")
     return ap.parse_args()
 
 
@@ -282,14 +284,17 @@ def main():
     def step_value(timed=None):
         # the whole step is enqueued behind a stream gate before the device
         # starts it, so host scheduling noise stays outside the event window
-        eng.hold()
+        gate = not args.no_gate
+        if gate:
+            eng.hold()
         if timed is not None:
             timed[0].record(stream)
         eng.load_device(v["n"], roots, d_hss.data_ptr(), d_args.data_ptr(), v["maxarity"], d_rc.data_ptr())
         eng.run_async()
         if timed is not None:
             timed[1].record(stream)
-        eng.release()
+        if gate:
+            eng.release()
         st = eng.run_wait()
         if timed is not None and st["launches"] > 1:
             # a relaunch (arena growth) ran after the closing event: close the

@@ -276,6 +276,8 @@ struct trs_gpu_engine {
     volatile uint32_t* h_gate = nullptr;  // trs_gpu_hold / trs_gpu_release
     uint32_t* d_gate = nullptr;
     uint32_t* d_roots_out = nullptr;      // renumbered roots of the export
+    uint32_t* d_stage = nullptr;          // trs_gpu_load H2D staging
+    size_t stage_words = 0;
     uint32_t roots_out_cap = 0;
     bool exported = false;                // staging holds the export of the current state
     trs_gpu_sweep_record* d_trace = nullptr;
@@ -974,6 +976,7 @@ void trs_gpu_close(trs_gpu_engine* e) {
     if (e->ev_a) cudaEventDestroy(e->ev_a);
     if (e->ev_b) cudaEventDestroy(e->ev_b);
     cudaFree(e->d_roots_out);
+    cudaFree(e->d_stage);
     if (e->load_a) cudaEventDestroy(e->load_a);
     if (e->load_b) cudaEventDestroy(e->load_b);
     cudaStreamDestroy(e->stream);
@@ -997,18 +1000,25 @@ int trs_gpu_load(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t 
                  const uint32_t* args, uint32_t max_arity, const uint32_t* refcounts, uint64_t capacity) {
     if (!e || !hss || !refcounts || (max_arity && !args) || !roots) return TRS_GPU_INVALID;
     cudaSetDevice(e->device);
-    uint32_t *dh = nullptr, *da = nullptr, *dr = nullptr;
-    size_t na = (size_t)max_arity * n;
-    CUDA_TRY(e, cudaMallocAsync(&dh, sizeof(uint32_t) * n, e->stream));
-    CUDA_TRY(e, cudaMallocAsync(&da, sizeof(uint32_t) * std::max<size_t>(na, 1), e->stream));
-    CUDA_TRY(e, cudaMallocAsync(&dr, sizeof(uint32_t) * n, e->stream));
+    // H2D into a grow-only staging buffer owned by the engine (no per-call
+    // allocation: allocator round trips show up as e2e jitter)
+    const size_t na = (size_t)max_arity * n;
+    const size_t words = (size_t)n * 2 + std::max<size_t>(na, 1);
+    if (e->stage_words < words) {
+        cudaFree(e->d_stage);
+        e->d_stage = nullptr;
+        e->stage_words = 0;
+        CUDA_TRY(e, cudaMalloc(&e->d_stage, sizeof(uint32_t) * words));
+        e->stage_words = words;
+    }
+    uint32_t* dh = e->d_stage;
+    uint32_t* dr = dh + n;
+    uint32_t* da = dr + n;
     CUDA_TRY(e, cudaMemcpyAsync(dh, hss, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e->stream));
     if (na) CUDA_TRY(e, cudaMemcpyAsync(da, args, sizeof(uint32_t) * na, cudaMemcpyHostToDevice, e->stream));
     CUDA_TRY(e, cudaMemcpyAsync(dr, refcounts, sizeof(uint32_t) * n, cudaMemcpyHostToDevice, e->stream));
     int rc = load_impl(e, n, roots, num_roots, dh, da, max_arity, dr, capacity);
-    cudaFreeAsync(dh, e->stream);
-    cudaFreeAsync(da, e->stream);
-    cudaFreeAsync(dr, e->stream);
+    // the caller may reuse its host buffers on return
     cudaStreamSynchronize(e->stream);
     return rc;
 }

@@ -6,3 +6,7 @@ timeout 1200 python -m pytest tests -x -q -m gpu --timeout 240 --timeout_method 
 tail -3 gpurun_out/pytest_gpu.log
 timeout 420 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/bench.log | head -c 3000
+if [ "$LAUNCHES" = "1" ]; then
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+      python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline --no-gate > /dev/null 2>&1; echo "launches rc=$?"
+fi
