@@ -198,15 +198,36 @@ def workload_config(args, nshards):
 
 
 def per_config_table(eng, api, W, counts, hbm_peak, gather_gbps):
-    """Single-GPU timing + parity of every BASELINE config (one warm-up, one timed run)."""
+    """Single-GPU timing + parity of every BASELINE config (one warm-up, one
+    timed run).  Rooflines: `gather_frac` is the SURVEY 8(d) model (4 B x A
+    against the measured uniformly random 4-B gather); it can exceed 1 where
+    part of the accesses hit L2 (build+sum: ~50 % L2 hit rate in ncu), so
+    `dram_frac` -- the ncu-measured DRAM bytes of the same launch
+    (profiles/traffic.json) over the run time, against the measured HBM copy
+    bandwidth -- is given beside it where a capture exists."""
+    import hashlib
+
     import torch
 
+    traffic = {}
+    if os.path.exists(PROFILE_SUMMARY):
+        with open(PROFILE_SUMMARY) as f:
+            traffic = json.load(f)
     out = {}
-    names = ["fib18", "mergesort16k", "transform22", "buildsum22", "reverse16k", "ackermann36"]
+    names = ["fib18", "mergesort16k", "transform22", "buildsum22", "reverse16k", "ackermann36", "sortbatch"]
     for name in names:
-        text = W.CONFIGS[name][0]()
-        sysm = api.System(text)
-        store = api.Store.load(sysm)
+        if name == "sortbatch":
+            texts = [W.treemergesort_batch(s) for s in range(1, 9)]
+            systems = [api.System(t) for t in texts]
+            sysm = systems[0]
+            store = api.Store.load(systems)
+            keys = [f"sortbatch_s{s}" for s in range(1, 9)]
+            tkey = "sortbatch_8shards"
+        else:
+            sysm = api.System(W.CONFIGS[name][0]())
+            store = api.Store.load(sysm)
+            keys = [name]
+            tkey = name
         eng.set_program(sysm)
         best = None
         for rep in range(2):
@@ -215,23 +236,28 @@ def per_config_table(eng, api, W, counts, hbm_peak, gather_gbps):
             best = st
         tr = eng.trace()
         widths = tr["rewrites"].astype("<u8")
-        import hashlib
-
-        c = counts.get(name)
+        cs = [counts.get(k) for k in keys]
         t = best["kernel_ms"] * 1e-3
         row = {"rewrites": best["total_rewrites"], "sweeps": best["sweeps"], "kernel_ms": best["kernel_ms"],
                "rewrites_per_s": best["total_rewrites"] / t, "us_per_sweep": 1e6 * t / best["sweeps"],
                "small_sweeps": best["small_sweeps"], "gc_runs": best["gc_runs"]}
-        if c:
-            row["parity_rewrites"] = c["rewrites"] == best["total_rewrites"]
-            row["parity_widths"] = c["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
-            a = c["A"]
+        if all(cs):
+            row["parity_rewrites"] = sum(c["rewrites"] for c in cs) == best["total_rewrites"]
+            if len(cs) == 1:
+                row["parity_widths"] = cs[0]["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
+            else:
+                row["parity_sweeps"] = max(c["sweeps"] for c in cs) == best["sweeps"]
+            a = sum(c["A"] for c in cs)
+            smin = sum(c["S_min"] for c in cs)
             row["gather_gbps"] = 4 * a / t / 1e9
             row["gather_frac"] = row["gather_gbps"] / gather_gbps if gather_gbps else None
-            row["dram_model_gbps"] = (32 * a + c["S_min"]) / t / 1e9
+            row["dram_model_gbps"] = (32 * a + smin) / t / 1e9
             row["dram_model_frac"] = row["dram_model_gbps"] / hbm_peak
-            t_roof = max(4 * a / (gather_gbps * 1e9) if gather_gbps else 0, c["S_min"] / (hbm_peak * 1e9))
+            t_roof = max(4 * a / (gather_gbps * 1e9) if gather_gbps else 0, smin / (hbm_peak * 1e9))
             row["t_roof_frac"] = t_roof / t
+        if tkey in traffic:
+            row["dram_gbps"] = traffic[tkey] / t / 1e9
+            row["dram_frac"] = row["dram_gbps"] / hbm_peak
         out[name] = row
         del store, sysm
         torch.cuda.synchronize()

@@ -232,8 +232,9 @@ void* trs_gpu_stream(trs_gpu_engine* engine);
  * profiled warp in match, claim, apply, push, whole sweep; sweeps; warp
  * steps; spare; match sub-phases record, children, slots, rules; then the
  * collector's phase ns (claim, count, scatter, remap), cascade hops and the
- * longest cascade. */
-int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out18);
+ * longest cascade; then, per profiled grid sweep summed, the maxima over
+ * warps of match, claim, apply, push, record, children, slots, rules. */
+int trs_gpu_profile_counters(trs_gpu_engine* engine, uint64_t* out26);
 
 /* Fixed per-sweep overhead probe on the loaded store: `iters` grid barriers
  * (mode 0) or barriers plus the frontier-table staging of a grid sweep

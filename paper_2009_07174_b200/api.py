@@ -467,11 +467,13 @@ class Engine:
         return ns.value
 
     def profile_counters(self) -> dict:
-        out = np.zeros(18, np.uint64)
+        out = np.zeros(26, np.uint64)
         lib().trs_gpu_profile_counters(self._h, out.ctypes.data)
         keys = ("match", "claim", "apply", "push", "sweep", "sweeps", "steps", "spare",
                 "m_record", "m_children", "m_slots", "m_rules",
-                "gc_claim_ns", "gc_count_ns", "gc_scatter_ns", "gc_remap_ns", "gc_hops", "gc_max_hops")
+                "gc_claim_ns", "gc_count_ns", "gc_scatter_ns", "gc_remap_ns", "gc_hops", "gc_max_hops",
+                "wmax_match", "wmax_claim", "wmax_apply", "wmax_push", "wmax_record", "wmax_children",
+                "wmax_slots", "wmax_rules")
         return {k: int(v) for k, v in zip(keys, out)}
 
     def compact(self, max_rounds: int = 8) -> dict:

@@ -65,6 +65,11 @@ struct Ctl {
     // profiling build: collection phase ns (claim, count, scatter, remap),
     // cascade hops, longest cascade
     unsigned long long gcprof[6];
+    // profiling build: per-sweep maxima over warps of the warp-step phases
+    // (match, claim, apply, push, record, children, slots, rules), rotating
+    // slots, and their sums over the profiled sweeps
+    unsigned long long wmax[2][8];
+    unsigned long long wmax_sum[8];
 };
 
 struct Params {

@@ -955,7 +955,9 @@ int trs_gpu_open(int device, trs_gpu_engine** out) {
     }
     cudaDeviceGetAttribute(&e->sm_count, cudaDevAttrMultiProcessorCount, device);
     // experimental frontier format (sweep.cuh, rich entries); off by default
+#if TRS_B200_RICH_ENTRIES
     if (const char* r = std::getenv("TRS_B200_RICH_ENTRIES")) e->rich = std::atoi(r) ? 1u : 0u;
+#endif
     int coop = 0;
     cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device);
     if (!coop || cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess) {
@@ -1055,6 +1057,7 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.debug_flags = opt.reserved[0];
     P.local_cap = e->resident_on ? resident_slots(e) : 0u;
     P.local_enter = P.local_cap / 2;
+    if (opt.reserved[2]) P.slab = opt.reserved[2];  // experiment: slab override
     void* args[] = {&P};
     cudaEventRecord(R.a, e->stream);
     prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);
@@ -1242,15 +1245,16 @@ int trs_gpu_release(trs_gpu_engine* e) {
 
 void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr; }
 
-int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out18) {
-    if (!e || !e->d_ctl || !out18) return TRS_GPU_INVALID;
-    uint64_t* out12 = out18;
+int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out26) {
+    if (!e || !e->d_ctl || !out26) return TRS_GPU_INVALID;
+    uint64_t* out12 = out26;
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     for (int k = 0; k < 12; ++k) out12[k] = c.prof[k];
     for (int k = 0; k < 6; ++k) out12[12 + k] = c.gcprof[k];
+    for (int k = 0; k < 8; ++k) out12[18 + k] = c.wmax_sum[k];
     return TRS_GPU_OK;
 }
 

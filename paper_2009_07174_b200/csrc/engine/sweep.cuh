@@ -47,6 +47,12 @@ struct StepCtx {
 // (libtrs_b200_prof.so, -DTRS_B200_PROFILE=1) so that the production step
 // loop carries none of its registers.
 constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
+// The rich frontier-entry format (record payloads in the list) is compiled
+// only on request (-DTRS_B200_RICH_ENTRIES=1): its extra inlined copy of the
+// warp step doubles the grid sweep's code for an opt-in format.
+#ifndef TRS_B200_RICH_ENTRIES
+#define TRS_B200_RICH_ENTRIES 0
+#endif
 
 struct PhaseClock {
     long long t[4] = {0, 0, 0, 0};  // match, claim, apply, push (debug accounting)
@@ -558,7 +564,7 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
         const uint32_t v = k * q + lane;
         const bool valid = lane < q && v < F.M;
         const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * (kRich ? W : 1) : in;
-        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && warp == 0, pc);
+        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc);
     }
     return lane == 0 ? rw : 0ull;
 }
@@ -1122,11 +1128,37 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr,
                   P.capacity, P.slab};
         PhaseClock pc;
+#if TRS_B200_PROFILE
+        // profiling build: the slowest warp's entry time of this sweep
+        // (max over the grid, rotating slot) lands in the trace's free_len,
+        // and per-phase maxima over warps in ctl->wmax
+        if (leader) {
+            ctl->gcprof[(s + 1) & 1] = 0;
+            for (int k = 0; k < 8; ++k) ctl->wmax[(s + 1) & 1][k] = 0;
+        }
+        const long long wt0 = clock64();
+        PhaseClock wpc;
+        const bool wprof = profsw && (threadIdx.x & 31) == 0;
+#else
+        PhaseClock& wpc = pc;
+        const bool wprof = profsw && leader;
+#endif
         unsigned long long rw =
+#if TRS_B200_RICH_ENTRIES
             P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                          profsw && leader, pc)
-                   : cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                           profsw && leader, pc);
+                                          wprof, wpc)
+                   :
+#endif
+                     cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
+                                           wprof, wpc);
+#if TRS_B200_PROFILE
+        if ((threadIdx.x & 31) == 0) atomicMax(&ctl->gcprof[s & 1], (unsigned long long)(clock64() - wt0));
+        if (wprof) {
+            for (int k = 0; k < 4; ++k) atomicMax(&ctl->wmax[s & 1][k], (unsigned long long)wpc.t[k]);
+            for (int k = 0; k < 4; ++k) atomicMax(&ctl->wmax[s & 1][4 + k], (unsigned long long)wpc.sub[k]);
+        }
+        if (leader) pc = wpc;
+#endif
         rw = block_sum64(rw, sm);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
@@ -1146,6 +1178,11 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         L.sweep = s;
         if (leader) {
             record(P, s, width, L, m, 0, global_ns() - t0);
+#if TRS_B200_PROFILE
+            if (s - L.sweep0 <= P.trace_cap && s > L.sweep0) P.trace[s - L.sweep0 - 1].free_len = (uint32_t)__ldcg(&ctl->gcprof[s & 1]);
+            if (profsw)
+                for (int k = 0; k < 8; ++k) ctl->wmax_sum[k] += __ldcg(&ctl->wmax[s & 1][k]);
+#endif
             if (profsw) {
                 for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
                 ctl->prof[4] += clock64() - cs;

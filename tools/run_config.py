@@ -82,7 +82,9 @@ def main():
         print(json.dumps({"cycles_per_sweep": {k: pc[k] / n for k in ("match", "claim", "apply", "push", "sweep")},
                           "cycles_per_warp_step": {k: round(pc[k] / ns) for k in ("match", "claim", "apply", "push", "m_record",
                                                                                   "m_children", "m_slots", "m_rules")},
-                          "profiled_sweeps": pc["sweeps"], "warp_steps": pc["steps"]}), flush=True)
+                          "profiled_sweeps": pc["sweeps"], "warp_steps": pc["steps"],
+                          "max_over_warps_per_sweep": {k[5:]: round(pc[k] / n) for k in pc if k.startswith("wmax_")}}),
+              flush=True)
     if args.trace_out:
         np.save(args.trace_out, res.trace)
     if args.ref:

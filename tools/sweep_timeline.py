@@ -27,6 +27,7 @@ def main():
     ap.add_argument("--variant", type=int, default=0)
     ap.add_argument("--debug-flags", type=int, default=0)
     ap.add_argument("--no-resident", action="store_true")
+    ap.add_argument("--slab", type=int, default=0)
     args = ap.parse_args()
     texts = texts_for(args.name)
     systems = [api.System(t) for t in texts]
@@ -36,6 +37,7 @@ def main():
     opts = api.make_options(variant=args.variant)
     opts.reserved[0] = args.debug_flags
     opts.reserved[1] = 1 if args.no_resident else 0
+    opts.reserved[2] = args.slab
     for _ in range(2):
         eng.load(store)
         st = eng.run(opts)
