@@ -104,6 +104,7 @@ struct Params {
     uint32_t debug_flags;   // experiments (trs_gpu_options.reserved[0])
     uint32_t local_cap;     // >0: slots of the shared-memory resident arena of the single-CTA mode
     uint32_t local_enter;   // allocated slots at or below which the single-CTA mode goes resident
+    uint32_t max_vars;      // binding columns in shared memory (largest rule's variable count)
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

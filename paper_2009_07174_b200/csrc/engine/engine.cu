@@ -252,6 +252,7 @@ struct trs_gpu_engine {
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
     bool resident_on = false;  // this run reserves the shared-memory resident arena
+    uint32_t max_vars = 1;     // binding columns the step loop keeps in shared memory
     uint32_t input_n = 0;      // slots of the loaded store
     uint32_t rich = 0;  // frontier entry format of the loaded store (fixed at load time)
 
@@ -617,6 +618,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     e->blob = std::move(blob);
     e->max_arity = max_arity;
     e->max_new = max_new;
+    e->max_vars = 1;
+    for (uint32_t r = 0; r < p->num_rules; ++r) e->max_vars = std::max<uint32_t>(e->max_vars, p->rules[r].num_vars);
     e->num_symbols = p->num_symbols;
     e->arity.assign(p->arity, p->arity + p->num_symbols);
     e->W = words_for_arity(max_arity);
@@ -649,7 +652,9 @@ const void* step_loop_for(int W, int minb) {
 // frontier lists, and (when enabled) the resident arena of the single-CTA
 // mode (sweep.cuh, run_small).
 constexpr size_t kSmemBudget = 227 * 1024 - 12 * 1024;  // dynamic bytes, leaving room for static smem
-size_t dyn_base(const trs_gpu_engine* e) { return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t); }
+size_t dyn_base(const trs_gpu_engine* e) {
+    return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t) + (size_t)e->max_vars * kBlock * sizeof(uint32_t);
+}
 uint32_t resident_slots(const trs_gpu_engine* e) {
     const size_t base = dyn_base(e);
     if (base >= kSmemBudget) return 0;
@@ -788,6 +793,7 @@ Params make_params(trs_gpu_engine* e, int blocks) {
     P.max_new = e->max_new;
     P.step_budget = 1000000000ull;
     P.rich = e->rich;
+    P.max_vars = e->max_vars;
     // slab: 256 slots per warp unless the arena is small
     uint64_t per_warp = e->capacity / (4ull * (uint64_t)blocks * kWarps);
     P.slab = (uint32_t)std::max<uint64_t>(16, std::min<uint64_t>(256, per_warp));

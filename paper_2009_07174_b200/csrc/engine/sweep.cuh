@@ -18,6 +18,20 @@
 
 namespace trs_b200 {
 
+// Variable bindings of the lane's chosen rule live in dynamic shared memory
+// (Params::max_vars columns of kBlock words, one column entry per thread:
+// bank-conflict free for equal indices).  As a dynamically indexed
+// per-thread array they would live in local memory, whose lines the random
+// gathers evict from L1, and every RHS reference to a variable would become
+// an L2 round trip on the rewrite's critical path.
+#define TRS_BIND(v) C.bind[(v) * kBlock]
+
+// Dynamic shared memory after the program: two frontier lists of the
+// single-CTA mode, the binding columns, then the resident arena.
+__device__ __forceinline__ uint32_t* bind_base(const Params& P, uint32_t* slist) {
+    return slist + 2 * kSmallCap + threadIdx.x;
+}
+
 enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild };
 
 struct Slab {
@@ -41,6 +55,7 @@ struct StepCtx {
     uint32_t* abort_flag; // shared flag raised with ctl->abort_capacity (may be null)
     uint64_t cap;         // slots of the arena being swept (global or shared-memory resident)
     uint32_t slab;        // fresh slots a warp claims at a time (0: exactly what a step needs)
+    uint32_t* bind;       // this thread's binding column (TRS_BIND)
 };
 
 // Phase cycle accounting is compiled only into the profiling build
@@ -96,7 +111,6 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     uint32_t act = kActNone;
     uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
     uint32_t a[MAXA];
-    uint32_t bind[kMaxVars];
     // level-synchronous matcher state (DPlan): children's first argument
     // quads, grandchild slot heads, and the argument quads of two slots
     uint32_t ch[MAXA];
@@ -242,7 +256,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                         const uint32_t node = src < kSrcSlot ? pick(a, src)
                                               : src < kSrcSArg ? pick(ca, src & 15u)
                                                                : pick(ga, src & 7u);
-                        bind[st.value] = node;
+                        TRS_BIND(st.value) = node;
                     }
                 }
                 if (ok) {
@@ -288,7 +302,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                             break;
                         }
                     } else {
-                        bind[st.value] = node;
+                        TRS_BIND(st.value) = node;
                     }
                 }
                 if (ok) {
@@ -371,7 +385,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         wval = kWoken;
     } else if (act == kActCollapse) {
         const DRule& Rl = G.rules[rule];
-        const uint32_t src = bind[Rl.root_ref];
+        const uint32_t src = TRS_BIND(Rl.root_ref);
         const uint32_t* S = rec<W>(arena, src);
         uint32_t shead, sar;
         uint32_t b[MAXA];
@@ -421,7 +435,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 b[j] = 0;
                 if ((uint32_t)j < iar) {
                     uint16_t ref = G.refs[I.first_ref + j];
-                    b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : bind[ref];
+                    b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : TRS_BIND(ref);
                 }
             }
             if (k < nfresh) {
@@ -509,7 +523,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                             b[j] = 0;
                             if ((uint32_t)j < iar) {
                                 const uint16_t ref = G.refs[I.first_ref + j];
-                                b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : bind[ref];
+                                b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : TRS_BIND(ref);
                             }
                         }
                         const uint32_t cur = root ? Rl.root_cursor : I.cursor;
@@ -831,7 +845,8 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             ss.claim = 0;
         }
         __syncwarp();
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size};
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
+                  bind_base(P, slist)};
         const bool valid = lane < m;
         const uint32_t width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
         __syncwarp();
@@ -886,7 +901,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     // these sweeps is a shared-memory access; claims are exact (no slabs),
     // a full resident arena is compacted in place (local_gc), and the store
     // moves back when the frontier outgrows this mode or stops fitting.
-    uint32_t* const resident_arena = slist + 2 * kSmallCap;
+    uint32_t* const resident_arena = slist + 2 * kSmallCap + P.max_vars * kBlock;
     bool resident = P.local_cap != 0 && L.bump <= P.local_enter;
     if (resident) {
         abandon_slab<W>(arena, slab);
@@ -951,7 +966,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         Frontier Fs{1, m, nullptr, nullptr};
         uint32_t zero_off = 0;
         Fs.off = &zero_off;
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size};
+        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
+                  bind_base(P, slist)};
         PhaseClock pc;
         unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
                                                       profc, pc);
@@ -1126,7 +1142,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
         StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr,
-                  P.capacity, P.slab};
+                  P.capacity, P.slab, bind_base(P, slist)};
         PhaseClock pc;
 #if TRS_B200_PROFILE
         // profiling build: the slowest warp's entry time of this sweep
