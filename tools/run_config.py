@@ -27,6 +27,10 @@ def texts_for(name: str):
         return W.batch_shards("fib")
     if name == "sortbatch":
         return W.batch_shards("sort")
+    if name.startswith("fibbatchN"):
+        return W.batch_shards("fib")[: int(name[len("fibbatchN"):])]
+    if name.startswith("sortbatchN"):
+        return W.batch_shards("sort")[: int(name[len("sortbatchN"):])]
     if name.startswith("fibbatch1"):
         return [W.fib_batch(1)]
     if name.startswith("sortbatch1"):
