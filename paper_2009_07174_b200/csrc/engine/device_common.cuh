@@ -243,6 +243,9 @@ struct Prog {
     const DInstr* instrs;
     const uint16_t* refs;
     const DPlan* plans;
+    const uint16_t* mrow;
+    const uint32_t* mtab;
+    uint32_t npos;
     uint32_t max_new;
 };
 
@@ -256,6 +259,9 @@ __device__ __forceinline__ Prog view_prog(const uint8_t* blob) {
     p.instrs = reinterpret_cast<const DInstr*>(blob + h->off_instrs);
     p.refs = reinterpret_cast<const uint16_t*>(blob + h->off_refs);
     p.plans = reinterpret_cast<const DPlan*>(blob + h->off_plans);
+    p.mrow = reinterpret_cast<const uint16_t*>(blob + h->off_mrow);
+    p.mtab = reinterpret_cast<const uint32_t*>(blob + h->off_mtab);
+    p.npos = h->npos;
     p.max_new = h->max_new_slots;
     return p;
 }

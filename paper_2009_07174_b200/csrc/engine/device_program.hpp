@@ -103,10 +103,19 @@ constexpr uint16_t kRefNode = 0x8000;
 // Symbols whose rules reach deeper (or past these limits) keep the
 // interpreted matcher (fast = 0).
 constexpr uint8_t kSrcChild = 0x00, kSrcSlot = 0x40, kSrcCArg = 0x80, kSrcSArg = 0xC0;
+constexpr uint8_t kPlanFast = 1, kPlanTables = 2;
+constexpr uint16_t kNoRow = 0xFFFF;
+// Match tables (planned symbols with <= 32 rules): rule choice without
+// walking the rules.  Every CheckHead of a planned symbol reads a position
+// -- child c's head (position c) or slot s's head (position rec_args(W)+s) --
+// and row[p][h] is the mask of the symbol's rules that accept head h at
+// position p (rules not checking p accept every h).  The first rule in
+// source order whose checks all hold (dispatch.hpp:119-130) is the lowest
+// bit of the AND over the checked positions.
 constexpr uint32_t kPlanSlots = 2, kPlanArgSlots = 1, kPlanChildren = 2;
 
 struct DPlan {
-    uint8_t fast;
+    uint8_t fast;        // bit 0: planned loads; bit 1: rule choice by match tables
     uint8_t child_args;  // bit j: load child j's first argument quad
     uint8_t nslots;
     uint8_t slot_args;   // bit s (s < kPlanArgSlots): load slot s's first argument quad
@@ -129,6 +138,9 @@ struct ProgHeader {
     uint32_t off_instrs;      // DInstr[]
     uint32_t off_refs;        // uint16_t[]
     uint32_t off_plans;       // DPlan[num_symbols]
+    uint32_t off_mrow;        // uint16_t[num_symbols][npos]: match-table row per checked position, 0xFFFF none
+    uint32_t off_mtab;        // uint32_t rows of num_symbols rule masks
+    uint32_t npos;            // positions per symbol: rec_args(W) children + kPlanSlots slots (0: no tables)
     uint32_t bytes;           // total blob size (multiple of 16)
 };
 

@@ -571,6 +571,52 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     }
     std::vector<DPlan> plans(p->num_symbols);
     for (uint32_t f = 0; f < p->num_symbols; ++f) plans[f] = plan_symbol(p, f, steps, rules);
+    // match tables (device_program.hpp): only for W <= 16 and within a budget
+    const int Wl = words_for_arity(max_arity);
+    const uint32_t nsym = p->num_symbols;
+    const uint32_t npos = Wl <= 16 ? (uint32_t)rec_args(Wl) + kPlanSlots : 0u;
+    std::vector<uint16_t> mrow;
+    std::vector<uint32_t> mtab;
+    if (npos) {
+        mrow.assign((size_t)nsym * npos, kNoRow);
+        for (uint32_t f = 0; f < nsym; ++f) {
+            if (!(plans[f].fast & kPlanFast)) continue;
+            const uint32_t r0 = p->rule_begin[f], nr = p->rule_begin[f + 1] - r0;
+            if (nr == 0 || nr > 32) continue;
+            const uint32_t all = nr == 32 ? 0xFFFFFFFFu : (1u << nr) - 1u;
+            std::vector<std::vector<uint32_t>> rows(npos);
+            for (uint32_t r = 0; r < nr; ++r) {
+                const trs_gpu_rule& R = p->rules[r0 + r];
+                for (uint32_t t = 0; t < R.num_steps; ++t) {
+                    const DStep& d = steps[R.first_step + t];
+                    if (d.kind != 0) continue;
+                    const uint32_t pos = d.src < kSrcSlot ? d.src : (uint32_t)rec_args(Wl) + (d.src - kSrcSlot);
+                    if (pos >= npos || d.value >= nsym) continue;
+                    if (rows[pos].empty()) rows[pos].assign(nsym, all);
+                    for (uint32_t h = 0; h < nsym; ++h)
+                        if (h != d.value) rows[pos][h] &= ~(1u << r);
+                }
+            }
+            const size_t need = mtab.size();
+            bool ok = true;
+            for (uint32_t q = 0; q < npos && ok; ++q)
+                if (!rows[q].empty() && mtab.size() + nsym > 0xFFFE) ok = false;
+            if (!ok) continue;
+            (void)need;
+            for (uint32_t q = 0; q < npos; ++q) {
+                if (rows[q].empty()) continue;
+                mrow[(size_t)f * npos + q] = (uint16_t)mtab.size();
+                mtab.insert(mtab.end(), rows[q].begin(), rows[q].end());
+            }
+            plans[f].fast |= kPlanTables;
+        }
+        // stay inside the program budget: without tables every symbol keeps the rule walk
+        if (mtab.size() * 4 + mrow.size() * 2 > 16 * 1024) {
+            for (auto& pl : plans) pl.fast &= (uint8_t)~kPlanTables;
+            mrow.clear();
+            mtab.clear();
+        }
+    }
     for (uint32_t k = 0; k < p->num_refs; ++k) {
         uint32_t ref = p->refs[k];
         refs[k] = (ref & TRS_GPU_REF_NODE) ? (uint16_t)(kRefNode | (ref & 0x7fff)) : (uint16_t)ref;
@@ -600,6 +646,11 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     off = align16(off + 2 * p->num_refs);
     h.off_plans = off;
     off = align16(off + sizeof(DPlan) * p->num_symbols);
+    h.npos = mtab.empty() ? 0u : npos;
+    h.off_mrow = off;
+    off = align16(off + 2 * (uint32_t)mrow.size());
+    h.off_mtab = off;
+    off = align16(off + 4 * (uint32_t)mtab.size());
     h.bytes = off;
     if (h.bytes > kMaxProgramBytes) return fail(e, TRS_GPU_INVALID, "program blob above 40 KiB");
     std::vector<uint8_t> blob(h.bytes, 0);
@@ -615,6 +666,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!instrs.empty()) std::memcpy(blob.data() + h.off_instrs, instrs.data(), sizeof(DInstr) * instrs.size());
     if (!refs.empty()) std::memcpy(blob.data() + h.off_refs, refs.data(), 2 * refs.size());
     std::memcpy(blob.data() + h.off_plans, plans.data(), sizeof(DPlan) * plans.size());
+    if (!mrow.empty()) std::memcpy(blob.data() + h.off_mrow, mrow.data(), 2 * mrow.size());
+    if (!mtab.empty()) std::memcpy(blob.data() + h.off_mtab, mtab.data(), 4 * mtab.size());
     e->blob = std::move(blob);
     e->max_arity = max_arity;
     e->max_new = max_new;

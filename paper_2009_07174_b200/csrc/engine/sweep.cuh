@@ -240,28 +240,59 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             // first matching rule in source order (dispatch.hpp:119-130),
             // every step answered from registers
             int chosen = -1;
-            for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
-                const DRule& Rl = G.rules[r];
-                bool ok = true;
-                for (uint32_t t = 0; t < Rl.num_steps; ++t) {
-                    const DStep st = G.steps[Rl.first_step + t];
-                    const uint32_t src = st.src;
-                    if (st.kind == 0) {
-                        const uint32_t head = src < kSrcSlot ? pick(ch, src) : pick(gh, src & 3u);
-                        if (head != st.value) {
-                            ok = false;
-                            break;
-                        }
-                    } else {
-                        const uint32_t node = src < kSrcSlot ? pick(a, src)
-                                              : src < kSrcSArg ? pick(ca, src & 15u)
-                                                               : pick(ga, src & 7u);
-                        TRS_BIND(st.value) = node;
+            if (pl.fast & kPlanTables) {
+                // match tables: AND the rule masks of every checked position
+                // (static register reads, no walk over the rules), then bind
+                // the chosen rule's variables
+                const uint16_t* rows = G.mrow + sym * G.npos;
+                const uint32_t nr = G.rule_begin[sym + 1] - G.rule_begin[sym];
+                uint32_t mask = nr >= 32 ? 0xFFFFFFFFu : (1u << nr) - 1u;
+#pragma unroll
+                for (int q = 0; q < MAXA; ++q) {
+                    const uint16_t row = rows[q];
+                    if (row != kNoRow) mask &= G.mtab[row + ch[q]];
+                }
+#pragma unroll
+                for (int q = 0; q < (int)kPlanSlots; ++q) {
+                    const uint16_t row = rows[MAXA + q];
+                    if (row != kNoRow) mask &= G.mtab[row + gh[q]];
+                }
+                if (mask) {
+                    chosen = (int)(G.rule_begin[sym] + __ffs(mask) - 1);
+                    const DRule& Rl = G.rules[chosen];
+                    for (uint32_t t = 0; t < Rl.num_steps; ++t) {
+                        const DStep st = G.steps[Rl.first_step + t];
+                        if (st.kind == 0) continue;
+                        const uint32_t src = st.src;
+                        TRS_BIND(st.value) = src < kSrcSlot ? pick(a, src)
+                                             : src < kSrcSArg ? pick(ca, src & 15u)
+                                                              : pick(ga, src & 7u);
                     }
                 }
-                if (ok) {
-                    chosen = (int)r;
-                    break;
+            } else {
+                for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
+                    const DRule& Rl = G.rules[r];
+                    bool ok = true;
+                    for (uint32_t t = 0; t < Rl.num_steps; ++t) {
+                        const DStep st = G.steps[Rl.first_step + t];
+                        const uint32_t src = st.src;
+                        if (st.kind == 0) {
+                            const uint32_t head = src < kSrcSlot ? pick(ch, src) : pick(gh, src & 3u);
+                            if (head != st.value) {
+                                ok = false;
+                                break;
+                            }
+                        } else {
+                            const uint32_t node = src < kSrcSlot ? pick(a, src)
+                                                  : src < kSrcSArg ? pick(ca, src & 15u)
+                                                                   : pick(ga, src & 7u);
+                            TRS_BIND(st.value) = node;
+                        }
+                    }
+                    if (ok) {
+                        chosen = (int)r;
+                        break;
+                    }
                 }
             }
             if (chosen < 0) {
