@@ -448,8 +448,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         *reinterpret_cast<uint2*>(R) = make_uint2(shead, s);
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
-        for (int j = 0; j < MAXA; ++j)
-            if ((uint32_t)j < sar) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
+        for (int j = 0; j < MAXA; ++j) {
+            if ((uint32_t)j >= sar) break;
+            rc_update(rec<W>(arena, b[j]) + kWRc, 1);
+        }
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -461,22 +463,27 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             const DInstr I = G.instrs[Rl.first_instr + k];
             const uint32_t iar = G.arity[I.symbol];
             uint32_t b[MAXA];
+            uint32_t vmask = 0;  // argument positions bound to variables
+#pragma unroll
+            for (int j = 0; j < MAXA; ++j) b[j] = 0;
 #pragma unroll
             for (int j = 0; j < MAXA; ++j) {
-                b[j] = 0;
-                if ((uint32_t)j < iar) {
-                    uint16_t ref = G.refs[I.first_ref + j];
-                    b[j] = (ref & kRefNode) ? fresh + (ref & 0x7fff) : TRS_BIND(ref);
-                }
+                if ((uint32_t)j >= iar) break;
+                const uint16_t ref = G.refs[I.first_ref + j];
+                const bool var = !(ref & kRefNode);
+                b[j] = var ? TRS_BIND(ref) : fresh + (ref & 0x7fff);
+                vmask |= (uint32_t)var << j;
             }
             if (k < nfresh) {
                 uint32_t sub = I.subscriber == kNone ? 0u : I.subscriber == kRootSub ? i : fresh + I.subscriber;
                 uint32_t* F = rec<W>(arena, fresh + k);
                 *reinterpret_cast<uint4*>(F) = make_uint4(I.symbol | ((uint32_t)I.cursor << kSymBits), 0u, I.indegree, sub);
+                // argument quads past the arity are never read: leave them unwritten
 #pragma unroll
                 for (int q = 0; q < MAXA / 4; ++q)
-                    *reinterpret_cast<uint4*>(F + kWArgs + q * 4) =
-                        make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
+                    if ((uint32_t)(q * 4) < iar)
+                        *reinterpret_cast<uint4*>(F + kWArgs + q * 4) =
+                            make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
             } else {
                 uint32_t* R = rec<W>(arena, i);
                 R[kWHead] = I.symbol | ((uint32_t)Rl.root_cursor << kSymBits);
@@ -485,10 +492,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
 #pragma unroll
             for (int j = 0; j < MAXA; ++j) {
-                if ((uint32_t)j < iar) {
-                    uint16_t ref = G.refs[I.first_ref + j];
-                    if (!(ref & kRefNode)) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
-                }
+                if ((vmask >> j) == 0u) break;
+                if ((vmask >> j) & 1u) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
             }
         }
         push_mask = Rl.push_mask;
@@ -500,8 +505,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // the reference orders them; sweep_engine.cpp:255-256)
     if (rewrote) {
 #pragma unroll
-        for (int j = 0; j < MAXA; ++j)
-            if ((uint32_t)j < ar) rc_update(rec<W>(arena, a[j]) + kWRc, -1);
+        for (int j = 0; j < MAXA; ++j) {
+            if ((uint32_t)j >= ar) break;
+            rc_update(rec<W>(arena, a[j]) + kWRc, -1);
+        }
     }
     if (wword) {
         uint32_t old = atomicCAS(wword, wcmp, wval);
