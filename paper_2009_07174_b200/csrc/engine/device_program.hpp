@@ -26,7 +26,7 @@ constexpr uint8_t kRootSub = 0xFE;
 
 constexpr uint32_t kMaxRuleSteps = 48;
 constexpr uint32_t kMaxRuleInstrs = 32;
-constexpr uint32_t kMaxVars = 16;
+constexpr uint32_t kMaxVars = 48;  // binding columns live in dynamic shared memory (2 KB each)
 constexpr uint32_t kMaxProgramBytes = 40 * 1024;
 
 // record word layout (W words per slot, W = 8/16/32):

@@ -468,6 +468,9 @@ DPlan plan_symbol(const trs_gpu_program* p, uint32_t f, std::vector<DStep>& step
     return pl;
 }
 
+constexpr size_t kSmemBudget = 227 * 1024 - 12 * 1024;  // dynamic bytes, leaving room for static smem
+size_t dyn_base(const trs_gpu_engine* e);
+
 int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!p || !p->arity || !p->rule_begin) return fail(e, TRS_GPU_INVALID, "null program");
     if (p->num_symbols == 0 || p->num_symbols > (1u << 16) - 2)
@@ -673,6 +676,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     e->max_new = max_new;
     e->max_vars = 1;
     for (uint32_t r = 0; r < p->num_rules; ++r) e->max_vars = std::max<uint32_t>(e->max_vars, p->rules[r].num_vars);
+    if (dyn_base(e) > kSmemBudget)
+        return fail(e, TRS_GPU_INVALID, "program + binding columns exceed the step loop's shared memory");
     e->num_symbols = p->num_symbols;
     e->arity.assign(p->arity, p->arity + p->num_symbols);
     e->W = words_for_arity(max_arity);
@@ -704,7 +709,6 @@ const void* step_loop_for(int W, int minb) {
 // Dynamic shared memory of the step loop: program blob, the two single-CTA
 // frontier lists, and (when enabled) the resident arena of the single-CTA
 // mode (sweep.cuh, run_small).
-constexpr size_t kSmemBudget = 227 * 1024 - 12 * 1024;  // dynamic bytes, leaving room for static smem
 size_t dyn_base(const trs_gpu_engine* e) {
     return e->blob.size() + 2 * kSmallCap * sizeof(uint32_t) + (size_t)e->max_vars * kBlock * sizeof(uint32_t);
 }

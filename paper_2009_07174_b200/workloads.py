@@ -263,3 +263,29 @@ def batch_shards(kind: str, shards: int = 8) -> list[str]:
     if kind == "sort":
         return [treemergesort_batch(s) for s in range(1, shards + 1)]
     raise ValueError(kind)
+
+
+def wide(k: int, vals=(3, 2, 4, 1, 2, 5, 1)) -> str:
+    """A test family for wide records (not a BASELINE config): a k-ary symbol
+    W rotating its arguments (W = 16 words for k <= 8, 32 beyond), a depth-3
+    pattern (Q, interpreted matcher) and Peano addition (planned matcher)."""
+    xs = [f"x{j}" for j in range(1, k + 1)]
+    ts = ", ".join(["Nat"] * k)
+    lines = [f"sort Nat = struct Zero() | S(Nat) | P(Nat, Nat) | W({ts}) | D(Nat) | Q(Nat);",
+             "var " + " ".join(f"{x} : Nat;" for x in xs) + " y : Nat;",
+             "eqn",
+             "  P(Zero(), y) = y;",
+             "  P(S(x1), y) = S(P(x1, y));",
+             "  D(x1) = P(Q(x1), x1);",
+             "  Q(S(S(S(x1)))) = Q(x1);",
+             "  Q(S(S(Zero()))) = Zero();",
+             "  Q(x1) = x1;",
+             f"  W(Zero(), {', '.join(xs[1:])}) = P({xs[1]}, {xs[-1]});",
+             f"  W(S(x1), {', '.join(xs[1:])}) = W({', '.join(xs[1:])}, D(x1));"]
+
+    def w(off):
+        vs = [vals[(off + j) % len(vals)] for j in range(k - 1)] + [0]
+        return "W(" + ", ".join(peano(v) for v in vs) + ")"
+
+    lines.append(f"input P({w(0)}, P({w(1)}, {w(2)}));")
+    return "\n".join(lines) + "\n"

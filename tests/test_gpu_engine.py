@@ -211,6 +211,23 @@ def test_resident_mode_is_invisible(engine, name, gc_interval):
     assert outs[0].trace["mode"].max() >= 1
 
 
+@pytest.mark.parametrize("k", [3, 6, 10, 20])
+@pytest.mark.parametrize("mode", ["default", "grid_only", "gc3"])
+def test_wide_records_against_oracle(engine, k, mode):
+    """Wide symbols (W = 16 and 32 word records) and a depth-3 pattern (the
+    interpreted matcher) against the C oracle restatement of the reference."""
+    from oracle import oracle as port
+
+    text = W.wide(k)
+    o = port.run_text(text)
+    opts = {"default": {}, "grid_only": {"disable_small": 1}, "gc3": {"gc_interval": 3}}[mode]
+    res = run(engine, text, **opts)
+    assert res.total_rewrites == o.rewrites and res.sweeps == o.sweeps
+    np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
+    np.testing.assert_array_equal(res.words[0], o.words[0])
+    assert res.stats["record_words"] == (8 if k <= 4 else 16 if k <= 8 else 32)
+
+
 def test_trace_records(engine):
     # sweep_engine_tests.cpp:238-255
     res = run(engine, CASES["mergesort10_s3"]["text"])
