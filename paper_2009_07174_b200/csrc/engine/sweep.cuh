@@ -612,11 +612,37 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     const uint32_t gw = nblocks * kWarps;
     const uint32_t q = chunk_lanes(F.M, nblocks);
     unsigned long long rw = 0;
-    for (uint32_t k = block_rank * kWarps + warp; k * q < F.M; k += gw) {
+    if (kRich) {
+        for (uint32_t k = block_rank * kWarps + warp; k * q < F.M; k += gw) {
+            const uint32_t v = k * q + lane;
+            const bool valid = lane < q && v < F.M;
+            const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * W : in;
+            rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc);
+        }
+        return lane == 0 ? rw : 0ull;
+    }
+    // Dense entries, software-pipelined over a warp's chunks: the slot ids
+    // of the chunk after next are loaded, and the records of the next chunk
+    // prefetched into L2, while the current chunk derives -- a wide sweep
+    // hands each warp dozens of chunks, and their entry -> record chain would
+    // otherwise be paid in full, one chunk after another.
+    auto slot_of = [&](uint32_t kk) -> uint32_t {
+        const uint32_t v = kk * q + lane;
+        return (lane < q && v < F.M) ? in[frontier_phys(F, v)] : 0u;  // generic: the list may be shared memory
+    };
+    uint32_t k = block_rank * kWarps + warp;
+    uint32_t s0 = k * q < F.M ? slot_of(k) : 0u;
+    uint32_t s1 = (k + gw) * q < F.M ? slot_of(k + gw) : 0u;
+    for (; k * q < F.M; k += gw) {
+        const uint32_t s2 = (k + 2 * gw) * q < F.M ? slot_of(k + 2 * gw) : 0u;
+        // generic prefetch: a no-op when the arena is the shared-memory resident one
+        if (s1) asm volatile("prefetch.L2 [%0];" ::"l"(rec<W>(arena, s1)));
         const uint32_t v = k * q + lane;
         const bool valid = lane < q && v < F.M;
-        const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * (kRich ? W : 1) : in;
-        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc);
+        const uint32_t slot = s0;
+        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, &slot, prof && (TRS_B200_PROFILE || warp == 0), pc);
+        s0 = s1;
+        s1 = s2;
     }
     return lane == 0 ? rw : 0ull;
 }
