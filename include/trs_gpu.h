@@ -118,7 +118,8 @@ typedef struct trs_gpu_options {
     uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters); >1: only grid sweeps of <= profile entries */
     uint32_t disable_warp_mode; /* 1: frontiers <= 32 slots still run on the whole CTA */
     uint32_t reserved[4];       /* [0] experiment flags (0); [1] bit 0: no shared-memory resident arena in
-                                   the single-CTA mode; [2..3] zero */
+                                   the single-CTA mode, bit 1: interpreted (not specialised) step loop;
+                                   [2] slab override (0); [3] zero */
 } trs_gpu_options;
 
 /* Per-sweep record (reference SweepRecord, sweep_engine.hpp:10-17).
@@ -155,6 +156,10 @@ typedef struct trs_gpu_stats {
     double load_ms;            /* device time of the load kernel */
 } trs_gpu_stats;
 
+/* The entry points below are host functions; the device code of the
+ * per-program specialisation (NVRTC) includes this header for the types only. */
+#ifndef __CUDACC_RTC__
+
 /* Number of visible CUDA devices (0 when none / no driver). */
 int trs_gpu_device_count(void);
 
@@ -166,7 +171,7 @@ const char* trs_gpu_last_error(trs_gpu_engine* engine);
 
 /* Stage the flattened DispatchTable in device memory (replaces the previous
  * program).  TRS_GPU_INVALID for a malformed program or one beyond the
- * device limits (max arity 28, 32 instructions / 48 steps / 16 vars per
+ * device limits (max arity 28, 32 instructions / 48 steps / 48 vars per
  * rule, program blob <= 40 KiB). */
 int trs_gpu_set_program(trs_gpu_engine* engine, const trs_gpu_program* program);
 
@@ -197,6 +202,14 @@ int trs_gpu_run(trs_gpu_engine* engine, const trs_gpu_options* options, trs_gpu_
  * One pending run per engine. */
 int trs_gpu_run_async(trs_gpu_engine* engine, const trs_gpu_options* options);
 int trs_gpu_run_wait(trs_gpu_engine* engine, trs_gpu_stats* stats);
+
+/* Per-program specialisation (the paper's generated rewrite functions,
+ * PAPER.md:305-327): trs_gpu_set_program compiles the step loop with the
+ * program's rule bindings and right-hand sides as straight-line code (NVRTC);
+ * TRS_B200_JIT=0 in the environment keeps the interpreted kernel, and
+ * trs_gpu_options.reserved[1] bit 1 selects it for one run.  Reports whether
+ * the specialised kernel is active, its compile time and the compiler log. */
+int trs_gpu_jit_info(trs_gpu_engine* engine, int* active, double* seconds, char* log, uint64_t log_cap);
 
 /* Stream gate: _hold enqueues a wait on a host-mapped flag so a whole step
  * (load + run) can be enqueued before the device starts it; _release opens
@@ -261,6 +274,8 @@ int trs_gpu_fetch_records(trs_gpu_engine* engine, void* dst, uint64_t cap_bytes,
  * counting bytes_per_access per access. */
 int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters,
                          double* gbps);
+
+#endif /* __CUDACC_RTC__ */
 
 #ifdef __cplusplus
 }

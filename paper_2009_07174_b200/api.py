@@ -124,6 +124,7 @@ def lib():
         "trs_gpu_run_async": ([P, ctypes.POINTER(Options)], I),
         "trs_gpu_run_wait": ([P, ctypes.POINTER(Stats)], I),
         "trs_gpu_hold": ([P], I),
+        "trs_gpu_jit_info": ([P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, U64], I),
         "trs_gpu_release": ([P], I),
         "trs_gpu_trace": ([P, P, U64, ctypes.POINTER(U64)], I),
         "trs_gpu_canonical": ([P, U32, P, U64, ctypes.POINTER(U64), u32p], I),
@@ -170,7 +171,7 @@ def exported_symbols() -> list[str]:
     return [n for n in ("trs_gpu_device_count", "trs_gpu_open", "trs_gpu_close", "trs_gpu_error_string",
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
                         "trs_gpu_run", "trs_gpu_run_async", "trs_gpu_run_wait", "trs_gpu_hold",
-                        "trs_gpu_release", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
+                        "trs_gpu_release", "trs_gpu_jit_info", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
                         "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
                         "trs_gpu_profile_counters", "trs_gpu_overhead_probe")]
 
@@ -448,6 +449,14 @@ class Engine:
         rc = lib().trs_gpu_run_wait(self._h, ctypes.byref(st))
         _raise(rc, self._err())
         return st.as_dict()
+
+    def jit_info(self) -> dict:
+        """Whether set_program compiled the specialised step loop (jit.hpp)."""
+        act = ctypes.c_int(0)
+        sec = ctypes.c_double(0)
+        log = ctypes.create_string_buffer(1 << 16)
+        _raise(lib().trs_gpu_jit_info(self._h, ctypes.byref(act), ctypes.byref(sec), log, len(log)), self._err())
+        return {"active": bool(act.value), "seconds": sec.value, "log": log.value.decode(errors="replace")}
 
     def hold(self):
         _raise(lib().trs_gpu_hold(self._h), self._err())

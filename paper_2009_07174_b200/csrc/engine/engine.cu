@@ -34,6 +34,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -44,6 +45,7 @@
 #include "device_program.hpp"
 #include "sweep.cuh"
 #include "export.cuh"
+#include "jit.hpp"
 #include "trs_gpu.h"
 
 using namespace trs_b200;
@@ -252,6 +254,10 @@ struct trs_gpu_engine {
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
     bool resident_on = false;  // this run reserves the shared-memory resident arena
+    const void* jit_kernel = nullptr;  // the program's specialised step loop (jit.hpp), if compiled
+    bool jit_off = false;              // this run uses the interpreted step loop
+    double jit_seconds = 0;
+    std::string jit_log;
     uint32_t max_vars = 1;     // binding columns the step loop keeps in shared memory
     uint32_t input_n = 0;      // slots of the loaded store
     uint32_t rich = 0;  // frontier entry format of the loaded store (fixed at load time)
@@ -736,10 +742,18 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     return TRS_GPU_OK;
 }
 
+// The step loop of this engine's next launch: the program's specialised
+// kernel when one was compiled (and not switched off for the run), else the
+// interpreted kernel of the record width.
+const void* loop_kernel(const trs_gpu_engine* e) {
+    if (e->jit_kernel && e->minb == 1 && !e->jit_off) return e->jit_kernel;
+    return step_loop_for(e->W, e->minb);
+}
+
 int grid_blocks(trs_gpu_engine* e, uint32_t blocks_per_sm) {
     int occ = 0;
     size_t dyn = dyn_smem(e);
-    const void* fn = step_loop_for(e->W, e->minb);
+    const void* fn = loop_kernel(e);
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, dyn) != cudaSuccess || occ < 1)
         occ = 1;
@@ -1058,6 +1072,31 @@ int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
     CUDA_TRY(e, cudaMalloc(&e->d_prog, e->blob.size()));
     CUDA_TRY(e, cudaMemcpy(e->d_prog, e->blob.data(), e->blob.size(), cudaMemcpyHostToDevice));
     e->loaded = false;
+    // specialise the step loop for this program (jit.hpp); TRS_B200_JIT=0
+    // keeps the interpreted kernel, and a failed compilation falls back to it
+    e->jit_kernel = nullptr;
+    e->jit_log.clear();
+    e->jit_seconds = 0;
+    const char* env = std::getenv("TRS_B200_JIT");
+    if (!(env && env[0] == '0')) {
+        const auto t0 = std::chrono::steady_clock::now();
+        JitResult jr = jit_compile(jit_source(e->blob.data(), e->W, e->max_vars), e->W);
+        e->jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        e->jit_kernel = jr.kernel;
+        e->jit_log = jr.log;
+    }
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_jit_info(trs_gpu_engine* e, int* active, double* seconds, char* log, uint64_t log_cap) {
+    if (!e) return TRS_GPU_INVALID;
+    if (active) *active = e->jit_kernel ? 1 : 0;
+    if (seconds) *seconds = e->jit_seconds;
+    if (log && log_cap) {
+        const size_t n = std::min<size_t>(e->jit_log.size(), log_cap - 1);
+        std::memcpy(log, e->jit_log.data(), n);
+        log[n] = 0;
+    }
     return TRS_GPU_OK;
 }
 
@@ -1125,7 +1164,7 @@ int enqueue_launch(trs_gpu_engine* e) {
     cudaEventRecord(R.a, e->stream);
     prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);
     cudaError_t err =
-        cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), R.blocks, kBlock, args, dyn_smem(e), e->stream);
+        cudaLaunchCooperativeKernel(loop_kernel(e), R.blocks, kBlock, args, dyn_smem(e), e->stream);
     if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_ctl, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream);
     cudaEventRecord(R.b, e->stream);
     R.launches++;
@@ -1149,6 +1188,7 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     R = RunState{};
     if (opt_in) R.opt = *opt_in;
     e->minb = R.opt.variant == 2 ? 2 : 1;
+    e->jit_off = (R.opt.reserved[1] & 2u) != 0;
     // the resident arena costs L1 capacity on every grid sweep: reserve it
     // only for stores small enough to start resident (single-term runs)
     e->resident_on = !(R.opt.reserved[1] & 1u) && resident_slots(e) != 0 && e->input_n <= resident_slots(e) / 2;
@@ -1337,7 +1377,7 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
     cudaEventCreate(&b);
     cudaEventRecord(a, e->stream);
     reset_barrier(e);
-    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
+    cudaError_t err = cudaLaunchCooperativeKernel(loop_kernel(e), blocks, kBlock, args, dyn_smem(e), e->stream);
     cudaEventRecord(b, e->stream);
     if (err == cudaSuccess) err = cudaEventSynchronize(b);
     float ms = 0.f;
@@ -1373,7 +1413,7 @@ int trs_gpu_overhead_probe(trs_gpu_engine* e, uint32_t iters, uint32_t mode, uin
     P.probe_mode = mode;
     void* args[] = {&P};
     reset_barrier(e);
-    cudaError_t err = cudaLaunchCooperativeKernel(step_loop_for(e->W, e->minb), blocks, kBlock, args, dyn_smem(e), e->stream);
+    cudaError_t err = cudaLaunchCooperativeKernel(loop_kernel(e), blocks, kBlock, args, dyn_smem(e), e->stream);
     if (err == cudaSuccess) err = cudaStreamSynchronize(e->stream);
     if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("probe: ") + cudaGetErrorString(err));
     Ctl c;

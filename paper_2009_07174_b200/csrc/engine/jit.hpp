@@ -1,0 +1,218 @@
+// Per-program specialisation of the step loop (host side).
+//
+// The paper generated one `rewrite_f` device function per symbol from each
+// TRS and compiled it with nvcc.  Here the same idea
+// runs at set_program: from the flattened program (the DispatchTable of
+// dispatch.hpp:73-78 as the blob of device_program.hpp) this emits
+//   gen_bind   -- the chosen rule's variable bindings as register moves
+//                 (constant indices into the matcher's register arrays),
+//   gen_csrc   -- a collapsing rule's source variable,
+//   gen_build  -- a constructive rule's right-hand side as straight-line
+//                 record stores and reference additions,
+// and NVRTC compiles them into the step loop (sweep.cuh with TRS_GEN = 1).
+// Everything else -- rule choice by match tables, claims, waiters, pushes,
+// collections -- is the same code as the interpreted kernel, so the two are
+// interchangeable launch by launch.
+#pragma once
+
+#include <nvrtc.h>
+
+#include <cstdio>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "device_program.hpp"
+
+namespace trs_b200_jit {
+extern const int kNumHeaders;
+extern const char* const kHeaderNames[];
+extern const char* const kHeaderSources[];
+}  // namespace trs_b200_jit
+
+namespace trs_b200 {
+
+struct BlobView {
+    const ProgHeader* h;
+    const uint8_t* arity;
+    const uint16_t* rule_begin;
+    const DRule* rules;
+    const DStep* steps;
+    const DInstr* instrs;
+    const uint16_t* refs;
+    const DPlan* plans;
+    explicit BlobView(const uint8_t* blob) {
+        h = reinterpret_cast<const ProgHeader*>(blob);
+        arity = blob + h->off_arity;
+        rule_begin = reinterpret_cast<const uint16_t*>(blob + h->off_rule_begin);
+        rules = reinterpret_cast<const DRule*>(blob + h->off_rules);
+        steps = reinterpret_cast<const DStep*>(blob + h->off_steps);
+        instrs = reinterpret_cast<const DInstr*>(blob + h->off_instrs);
+        refs = reinterpret_cast<const uint16_t*>(blob + h->off_refs);
+        plans = reinterpret_cast<const DPlan*>(blob + h->off_plans);
+    }
+};
+
+inline std::string jit_src_expr(uint8_t src) {
+    char b[32];
+    if (src < kSrcSlot)
+        std::snprintf(b, sizeof b, "a[%u]", (unsigned)src);
+    else if (src < kSrcSArg)
+        std::snprintf(b, sizeof b, "ca[%u]", (unsigned)(src & 15u));
+    else
+        std::snprintf(b, sizeof b, "ga[%u]", (unsigned)(src & 7u));
+    return b;
+}
+
+// CUDA source of the specialised step loop for record width W.
+inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
+    const BlobView B(blob);
+    const uint32_t nsym = B.h->num_symbols;
+    const int MAXA = rec_args(W);
+    std::string bind, csrc, build;
+    char line[256];
+    for (uint32_t f = 0; f < nsym; ++f) {
+        for (uint32_t r = B.rule_begin[f]; r < B.rule_begin[f + 1]; ++r) {
+            const DRule& R = B.rules[r];
+            if (B.plans[f].fast & kPlanTables) {
+                std::string body;
+                for (uint32_t t = 0; t < R.num_steps; ++t) {
+                    const DStep& d = B.steps[R.first_step + t];
+                    if (d.kind == 0) continue;
+                    std::snprintf(line, sizeof line, " gb[%u] = %s;", d.value, jit_src_expr(d.src).c_str());
+                    body += line;
+                }
+                if (!body.empty()) bind += "        case " + std::to_string(r) + ":" + body + " break;\n";
+            }
+            if (R.collapse) {
+                std::snprintf(line, sizeof line, "        case %u: return gb[%u];\n", r, (unsigned)R.root_ref);
+                csrc += line;
+                continue;
+            }
+            // constructive: fresh nodes 0..new_slots-1, then the root in place
+            std::string body;
+            std::vector<uint32_t> var_refs;
+            for (uint32_t k = 0; k <= R.new_slots; ++k) {
+                const DInstr& I = B.instrs[R.first_instr + k];
+                const uint32_t iar = B.arity[I.symbol];
+                std::vector<std::string> args(MAXA, "0u");
+                for (uint32_t j = 0; j < iar; ++j) {
+                    const uint16_t ref = B.refs[I.first_ref + j];
+                    if (ref & kRefNode) {
+                        args[j] = "fresh + " + std::to_string(ref & 0x7fff) + "u";
+                    } else {
+                        args[j] = "gb[" + std::to_string(ref) + "]";
+                        var_refs.push_back(ref);
+                    }
+                }
+                if (k < R.new_slots) {
+                    std::string sub = I.subscriber == kNone ? "0u"
+                                      : I.subscriber == kRootSub ? "i"
+                                                                 : "fresh + " + std::to_string(I.subscriber) + "u";
+                    std::snprintf(line, sizeof line,
+                                  "            { uint32_t* F = rec<W>(arena, fresh + %uu);\n"
+                                  "              *reinterpret_cast<uint4*>(F) = make_uint4(%uu, 0u, %uu, %s);\n",
+                                  k, I.symbol | ((uint32_t)I.cursor << kSymBits), (unsigned)I.indegree, sub.c_str());
+                    body += line;
+                    for (uint32_t q = 0; q * 4 < iar; ++q)
+                        body += "              *reinterpret_cast<uint4*>(F + kWArgs + " + std::to_string(q * 4) +
+                                ") = make_uint4(" + args[q * 4] + ", " + args[q * 4 + 1] + ", " + args[q * 4 + 2] +
+                                ", " + args[q * 4 + 3] + ");\n";
+                    body += "            }\n";
+                } else {
+                    std::snprintf(line, sizeof line,
+                                  "            { uint32_t* R = rec<W>(arena, i);\n"
+                                  "              R[kWHead] = %uu;\n"
+                                  "              const uint32_t b[%d] = {",
+                                  I.symbol | ((uint32_t)R.root_cursor << kSymBits), MAXA);
+                    body += line;
+                    for (int j = 0; j < MAXA; ++j) body += (j ? ", " : "") + args[j];
+                    body += "};\n              store_args<W>(R, b, ar > " + std::to_string(iar) + "u ? ar : " +
+                            std::to_string(iar) + "u);\n            }\n";
+                }
+            }
+            // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
+            for (uint32_t v : var_refs)
+                body += "            rc_update(rec<W>(arena, gb[" + std::to_string(v) + "]) + kWRc, 1);\n";
+            build += "        case " + std::to_string(r) + ": {\n" + body + "            break;\n        }\n";
+        }
+    }
+    std::string src;
+    src += "#define TRS_GEN 1\n#define TRS_GEN_MAXV " + std::to_string(max_vars) + "\n";
+    src += "#include \"device_common.cuh\"\nnamespace trs_b200 {\n";
+    src += "template <int W>\n__device__ __forceinline__ void gen_bind(uint32_t rule, const uint32_t (&a)[rec_args(W)],\n"
+           "    const uint32_t (&ca)[kPlanChildren * 4], const uint32_t (&ga)[kPlanArgSlots * 4],\n"
+           "    uint32_t (&gb)[TRS_GEN_MAXV]) {\n    switch (rule) {\n" +
+           bind + "        default: break;\n    }\n}\n";
+    src += "__device__ __forceinline__ uint32_t gen_csrc(uint32_t rule, const uint32_t (&gb)[TRS_GEN_MAXV]) {\n"
+           "    switch (rule) {\n" +
+           csrc + "        default: return 0u;\n    }\n}\n";
+    src += "template <int W>\n__device__ __forceinline__ void gen_build(uint32_t rule, uint32_t* arena, uint32_t fresh,\n"
+           "    uint32_t i, uint32_t ar, const uint32_t (&gb)[TRS_GEN_MAXV]) {\n    switch (rule) {\n" +
+           build + "        default: break;\n    }\n}\n}  // namespace trs_b200\n#include \"sweep.cuh\"\n";
+    return src;
+}
+
+struct JitResult {
+    const void* kernel = nullptr;
+    std::string log;
+    double seconds = 0;
+};
+
+// Compile (or fetch from the process-wide cache) the specialised step loop.
+inline JitResult jit_compile(const std::string& src, int W) {
+    static std::mutex mu;
+    static std::unordered_map<std::string, const void*> cache;
+    const std::string key = std::to_string(W) + "\n" + src;
+    {
+        std::lock_guard<std::mutex> g(mu);
+        auto it = cache.find(key);
+        if (it != cache.end()) return JitResult{it->second, "", 0};
+    }
+    JitResult out;
+    nvrtcProgram prog;
+    if (nvrtcCreateProgram(&prog, src.c_str(), "trs_gen.cu", trs_b200_jit::kNumHeaders, trs_b200_jit::kHeaderSources,
+                           trs_b200_jit::kHeaderNames) != NVRTC_SUCCESS) {
+        out.log = "nvrtcCreateProgram failed";
+        return out;
+    }
+    const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", 1>";
+    nvrtcAddNameExpression(prog, name.c_str());
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DTRS_B200_PROFILE=0"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+    size_t n = 0;
+    nvrtcGetProgramLogSize(prog, &n);
+    out.log.resize(n);
+    if (n) nvrtcGetProgramLog(prog, &out.log[0]);
+    if (rc != NVRTC_SUCCESS) {
+        nvrtcDestroyProgram(&prog);
+        return out;
+    }
+    const char* lowered = nullptr;
+    nvrtcGetLoweredName(prog, name.c_str(), &lowered);
+    const std::string lname = lowered ? lowered : "";
+    size_t cb = 0;
+    nvrtcGetCUBINSize(prog, &cb);
+    std::vector<char> cubin(cb);
+    nvrtcGetCUBIN(prog, cubin.data());
+    nvrtcDestroyProgram(&prog);
+    cudaLibrary_t lib = nullptr;
+    if (cudaLibraryLoadData(&lib, cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0) != cudaSuccess) {
+        out.log += "\ncudaLibraryLoadData failed";
+        cudaGetLastError();
+        return out;
+    }
+    cudaKernel_t k = nullptr;
+    if (cudaLibraryGetKernel(&k, lib, lname.c_str()) != cudaSuccess) {
+        out.log += "\ncudaLibraryGetKernel failed for " + lname;
+        cudaGetLastError();
+        return out;
+    }
+    out.kernel = reinterpret_cast<const void*>(k);
+    std::lock_guard<std::mutex> g(mu);
+    cache[key] = out.kernel;
+    return out;
+}
+
+}  // namespace trs_b200

@@ -62,6 +62,12 @@ struct StepCtx {
 // (libtrs_b200_prof.so, -DTRS_B200_PROFILE=1) so that the production step
 // loop carries none of its registers.
 constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
+// TRS_GEN: this translation unit is the per-program specialisation compiled
+// at set_program by NVRTC (engine.cu, jit_compile); the generated functions
+// gen_bind / gen_csrc / gen_build are defined before this header.
+#ifndef TRS_GEN
+#define TRS_GEN 0
+#endif
 // The rich frontier-entry format (record payloads in the list) is compiled
 // only on request (-DTRS_B200_RICH_ENTRIES=1): its extra inlined copy of the
 // warp step doubles the grid sweep's code for an opt-in format.
@@ -119,6 +125,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     uint32_t ga[kPlanArgSlots * 4];
     uint32_t cs_head = 0, cs_b[4] = {0, 0, 0, 0};  // collapse source record taken from registers
     uint32_t own_waiter = 0;  // the record's waiter word as loaded (the nf publication's first guess)
+#if TRS_GEN
+    bool gb_ready = false;       // set by the match-table path; the walks bind through shared memory
+    uint32_t gb[TRS_GEN_MAXV];  // the chosen rule's bindings, in registers (constant indices only)
+#pragma unroll
+    for (int v = 0; v < TRS_GEN_MAXV; ++v) gb[v] = 0;
+#endif
     bool planned = false;
     if (valid) {
         uint32_t headw;
@@ -259,6 +271,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 }
                 if (mask) {
                     chosen = (int)(G.rule_begin[sym] + __ffs(mask) - 1);
+#if TRS_GEN
+                    gen_bind<W>((uint32_t)chosen, a, ca, ga, gb);
+                    gb_ready = true;
+#else
                     const DRule& Rl = G.rules[chosen];
                     for (uint32_t t = 0; t < Rl.num_steps; ++t) {
                         const DStep st = G.steps[Rl.first_step + t];
@@ -268,6 +284,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                                              : src < kSrcSArg ? pick(ca, src & 15u)
                                                               : pick(ga, src & 7u);
                     }
+#endif
                 }
             } else {
                 for (uint32_t r = G.rule_begin[sym]; r < G.rule_begin[sym + 1]; ++r) {
@@ -349,6 +366,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             }
         }
     }
+#if TRS_GEN
+    if (!gb_ready && (act == kActCollapse || act == kActBuild)) {
+#pragma unroll
+        for (int v = 0; v < TRS_GEN_MAXV; ++v) gb[v] = TRS_BIND(v);
+    }
+#endif
     if (prof) pc.mark(3, act);
     long long c1 = prof ? clock64() : 0;
     if (prof) pc.t[0] += c1 - c0;
@@ -416,7 +439,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         wval = kWoken;
     } else if (act == kActCollapse) {
         const DRule& Rl = G.rules[rule];
+#if TRS_GEN
+        const uint32_t src = gen_csrc(rule, gb);
+#else
         const uint32_t src = TRS_BIND(Rl.root_ref);
+#endif
         const uint32_t* S = rec<W>(arena, src);
         uint32_t shead, sar;
         uint32_t b[MAXA];
@@ -458,6 +485,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         rewrote = true;
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
+#if TRS_GEN
+        gen_build<W>(rule, arena, fresh, i, ar, gb);
+#else
         const uint32_t nfresh = Rl.new_slots;
         for (uint32_t k = 0; k <= nfresh; ++k) {
             const DInstr I = G.instrs[Rl.first_instr + k];
@@ -496,6 +526,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 if ((vmask >> j) & 1u) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
             }
         }
+#endif
         push_mask = Rl.push_mask;
         npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
         push1 = i;
