@@ -254,6 +254,14 @@ struct trs_gpu_engine {
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
     bool resident_on = false;  // this run reserves the shared-memory resident arena
+    uint64_t pg_capacity = 0;  // prefer_grow() cache key (capacity, W) and value
+    int pg_W = 0;
+    bool pg_value = false;
+    // grid_blocks() cache: kernel, dynamic shared memory, blocks-per-SM cap -> blocks
+    const void* gb_fn = nullptr;
+    size_t gb_dyn = 0;
+    uint32_t gb_cap = 0;
+    int gb_blocks = 0;
     const void* jit_kernel = nullptr;  // the program's specialised step loop (jit.hpp), if compiled
     bool jit_off = false;              // this run uses the interpreted step loop
     double jit_seconds = 0;
@@ -754,11 +762,16 @@ int grid_blocks(trs_gpu_engine* e, uint32_t blocks_per_sm) {
     int occ = 0;
     size_t dyn = dyn_smem(e);
     const void* fn = loop_kernel(e);
+    if (fn == e->gb_fn && dyn == e->gb_dyn && blocks_per_sm == e->gb_cap && e->gb_blocks) return e->gb_blocks;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, dyn) != cudaSuccess || occ < 1)
         occ = 1;
     if (blocks_per_sm) occ = std::min<int>(occ, (int)blocks_per_sm);
-    return std::min<int>(occ * e->sm_count, (int)kMaxGrid);
+    e->gb_fn = fn;
+    e->gb_dyn = dyn;
+    e->gb_cap = blocks_per_sm;
+    e->gb_blocks = std::min<int>(occ * e->sm_count, (int)kMaxGrid);
+    return e->gb_blocks;
 }
 
 // Frontier of the next sweep (list buffer c.cur): total entries and the
@@ -875,14 +888,21 @@ Params make_params(trs_gpu_engine* e, int blocks) {
 // map of the grown store fit comfortably in free HBM; the compacting GC is
 // the memory-pressure path (and what fixed-capacity stores rely on).
 bool prefer_grow(trs_gpu_engine* e) {
-    size_t free_b = 0, total_b = 0;
-    if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
+    // cudaMemGetInfo can stall the host for milliseconds: ask once per
+    // capacity, not once per launch
+    if (e->pg_capacity != e->capacity || e->pg_W != e->W) {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
+            cudaGetLastError();
+            free_b = 0;
+        }
+        const uint64_t next = e->capacity * 2;
+        const uint64_t need = next * ((uint64_t)e->W * 4 * 2 + 4 * 3);
+        e->pg_value = need < free_b / 2;
+        e->pg_capacity = e->capacity;
+        e->pg_W = e->W;
     }
-    uint64_t next = e->capacity * 2;
-    uint64_t need = next * ((uint64_t)e->W * 4 * 2 + 4 * 3);
-    return need < free_b / 2;
+    return e->pg_value;
 }
 
 int grow_trace(trs_gpu_engine* e) {
@@ -1084,6 +1104,16 @@ int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
         e->jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         e->jit_kernel = jr.kernel;
         e->jit_log = jr.log;
+        if (e->jit_kernel) {
+            // load the module now (lazy loading would otherwise happen at the
+            // first launch, possibly behind a held stream gate)
+            cudaFuncAttributes fa;
+            if (cudaFuncGetAttributes(&fa, e->jit_kernel) != cudaSuccess) {
+                cudaGetLastError();
+                e->jit_kernel = nullptr;
+                e->jit_log += "\nspecialised kernel failed to load";
+            }
+        }
     }
     return TRS_GPU_OK;
 }
