@@ -164,7 +164,7 @@ struct JitResult {
 inline JitResult jit_compile(const std::string& src, int W) {
     static std::mutex mu;
     static std::unordered_map<std::string, const void*> cache;
-    const std::string key = std::to_string(W) + "\n" + src;
+    const std::string key = std::to_string(W) + (TRS_B200_PROFILE ? "p\n" : "\n") + src;
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -179,7 +179,9 @@ inline JitResult jit_compile(const std::string& src, int W) {
     }
     const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", 1>";
     nvrtcAddNameExpression(prog, name.c_str());
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo", "-DTRS_B200_PROFILE=0"};
+    // the specialisation is built like the library that loads it (profiling build or not)
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                          TRS_B200_PROFILE ? "-DTRS_B200_PROFILE=1" : "-DTRS_B200_PROFILE=0"};
     const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
