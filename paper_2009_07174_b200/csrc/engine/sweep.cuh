@@ -769,6 +769,51 @@ __device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nbloc
                                    uint32_t* f_off, Smem& sm, unsigned long long* width) {
     const uint32_t t0 = threadIdx.x, t1 = threadIdx.x + kBlock;
     const uint32_t R = __ldcg(&P.ctl->nregions[buf]);
+    if (nblocks <= kBlock) {
+        // one region per thread: warp scans, then warp 0 scans the warp totals
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        const uint32_t c = t0 < R ? __ldcg(region_cnt(P, buf) + t0) : 0u;
+        if (t0 < R) f_off[t0] = __ldcg(region_off(P, buf) + t0);
+        unsigned long long r = (width && t0 < R) ? __ldcg(P.region_rew + buf * kMaxGrid + t0) : 0ull;
+        uint32_t x = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+            r += __shfl_xor_sync(0xffffffffu, r, o);
+        }
+        __shared__ uint32_t wpre[kWarps + 1];
+        __shared__ unsigned long long wrw;
+        if (lane == 31) sm.scan[warp] = x;
+        if (lane == 0) sm.red[warp] = r;
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t v = lane < kWarps ? sm.scan[lane] : 0u;
+            unsigned long long rr = lane < kWarps ? sm.red[lane] : 0ull;
+            uint32_t xi = v;
+#pragma unroll
+            for (int o = 1; o < kWarps; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, xi, o);
+                if (lane >= o) xi += y;
+                rr += __shfl_xor_sync(0xffffffffu, rr, o);
+            }
+            if (lane < kWarps) wpre[lane] = xi - v;
+            if (lane == kWarps - 1) wpre[kWarps] = xi;
+            if (lane == 0) wrw = rr;
+        }
+        __syncthreads();
+        const uint32_t M = wpre[kWarps];
+        if (t0 < R) f_pref[t0] = wpre[warp] + x - c;
+        if (t0 == 0) f_pref[R] = M;
+        if (width) *width = wrw;
+        __syncthreads();
+        Frontier F;
+        F.R = R;
+        F.M = M;
+        F.pref = f_pref;
+        F.off = f_off;
+        return F;
+    }
     uint32_t c0 = t0 < nblocks ? __ldcg(region_cnt(P, buf) + t0) : 0u;
     uint32_t c1 = t1 < nblocks ? __ldcg(region_cnt(P, buf) + t1) : 0u;
     const uint32_t o0 = t0 < nblocks ? __ldcg(region_off(P, buf) + t0) : 0u;
