@@ -265,6 +265,7 @@ struct trs_gpu_engine {
     const void* jit_kernel = nullptr;  // the program's specialised step loop (jit.hpp), if compiled
     bool jit_off = false;              // this run uses the interpreted step loop
     double jit_seconds = 0;
+    int jit_minb = 1;
     std::string jit_log;
     uint32_t max_vars = 1;     // binding columns the step loop keeps in shared memory
     uint32_t input_n = 0;      // slots of the loaded store
@@ -754,7 +755,7 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
 // kernel when one was compiled (and not switched off for the run), else the
 // interpreted kernel of the record width.
 const void* loop_kernel(const trs_gpu_engine* e) {
-    if (e->jit_kernel && e->minb == 1 && !e->jit_off) return e->jit_kernel;
+    if (e->jit_kernel && !e->jit_off) return e->jit_kernel;
     return step_loop_for(e->W, e->minb);
 }
 
@@ -1100,7 +1101,11 @@ int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
     const char* env = std::getenv("TRS_B200_JIT");
     if (!(env && env[0] == '0')) {
         const auto t0 = std::chrono::steady_clock::now();
-        JitResult jr = jit_compile(jit_source(e->blob.data(), e->W, e->max_vars), e->W);
+        // experiment hook: the specialisation's register budget (MINB = 2 spills
+        // and measured 1.5-2x slower on every config; the default is 1)
+        const char* mb = std::getenv("TRS_B200_JIT_MINB");
+        e->jit_minb = (mb && mb[0] == '2') ? 2 : 1;
+        JitResult jr = jit_compile(jit_source(e->blob.data(), e->W, e->max_vars), e->W, e->jit_minb);
         e->jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         e->jit_kernel = jr.kernel;
         e->jit_log = jr.log;

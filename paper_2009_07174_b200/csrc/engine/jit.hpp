@@ -161,10 +161,10 @@ struct JitResult {
 };
 
 // Compile (or fetch from the process-wide cache) the specialised step loop.
-inline JitResult jit_compile(const std::string& src, int W) {
+inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     static std::mutex mu;
     static std::unordered_map<std::string, const void*> cache;
-    const std::string key = std::to_string(W) + (TRS_B200_PROFILE ? "p\n" : "\n") + src;
+    const std::string key = std::to_string(W) + "/" + std::to_string(minb) + (TRS_B200_PROFILE ? "p\n" : "\n") + src;
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -177,7 +177,7 @@ inline JitResult jit_compile(const std::string& src, int W) {
         out.log = "nvrtcCreateProgram failed";
         return out;
     }
-    const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", 1>";
+    const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", " + std::to_string(minb) + ">";
     nvrtcAddNameExpression(prog, name.c_str());
     // the specialisation is built like the library that loads it (profiling build or not)
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",

@@ -289,3 +289,26 @@ def test_full_size_batch_shard(engine):
     res = run(engine, W.treemergesort_batch(1))
     assert res.total_rewrites == c["rewrites"] and res.sweeps == c["sweeps"]
     assert _sha(res.widths) == c["widths_sha1"]
+
+
+def test_async_run_behind_stream_gate(engine):
+    """run_async + run_wait (with the whole step enqueued behind a stream
+    gate) gives the same result as run, and a second pending run is refused."""
+    g = CASES["mergesort64_s1"]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    engine.set_program(s)
+    engine.load(st)
+    engine.run()  # warm: modules loaded, arena sized
+    engine.load(st)
+    engine.hold()
+    engine.run_async()
+    with pytest.raises(ValueError):
+        engine.run_async()  # one pending run per engine
+    engine.release()
+    stats = engine.run_wait()
+    assert stats["total_rewrites"] == g["rewrites"]
+    np.testing.assert_array_equal(engine.trace()["rewrites"], np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
+    with pytest.raises(ValueError):
+        engine.run_wait()  # nothing pending
