@@ -289,3 +289,24 @@ def wide(k: int, vals=(3, 2, 4, 1, 2, 5, 1)) -> str:
 
     lines.append(f"input P({w(0)}, P({w(1)}, {w(2)}));")
     return "\n".join(lines) + "\n"
+
+
+def many_rules(nrules: int = 40, depth: int = 8) -> str:
+    """A test family (not a BASELINE config): one symbol with `nrules` rules
+    (past the 32-rule match tables, so its rule choice walks the rules) next
+    to ordinary planned symbols."""
+    cs = [f"C{k}()" for k in range(nrules + 1)]
+    lines = ["sort T = struct " + " | ".join(cs) + " | F(T) | G(T, T) | H(T);", "var x : T; y : T;", "eqn"]
+    for k in range(nrules):
+        lines.append(f"  F(C{k}()) = H(C{k + 1}());")
+    lines.append("  H(x) = x;")
+    lines.append("  G(C0(), y) = F(y);")
+    lines.append("  G(x, y) = F(x);")
+
+    def tree(d, k):
+        if d == 0:
+            return f"F(C{k % nrules}())"
+        return f"G({tree(d - 1, 2 * k)}, {tree(d - 1, 2 * k + 1)})"
+
+    lines.append(f"input {tree(depth, 1)};")
+    return "\n".join(lines) + "\n"

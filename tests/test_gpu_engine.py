@@ -228,6 +228,24 @@ def test_wide_records_against_oracle(engine, k, mode):
     assert res.stats["record_words"] == (8 if k <= 4 else 16 if k <= 8 else 32)
 
 
+@pytest.mark.parametrize("nrules", [8, 32, 40])
+@pytest.mark.parametrize("interp", [0, 2])
+def test_many_rules_against_oracle(engine, nrules, interp):
+    """A symbol with up to 40 rules (beyond the 32-rule match tables: rule
+    walk), with and without the per-program specialisation, against the C
+    oracle restatement of the reference."""
+    from oracle import oracle as port
+
+    text = W.many_rules(nrules)
+    o = port.run_text(text)
+    opts = api.make_options()
+    opts.reserved[1] = interp
+    res = api.normalize_texts(text, engine=engine, options=opts)
+    assert res.total_rewrites == o.rewrites and res.sweeps == o.sweeps
+    np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
+    np.testing.assert_array_equal(res.words[0], o.words[0])
+
+
 def test_trace_records(engine):
     # sweep_engine_tests.cpp:238-255
     res = run(engine, CASES["mergesort10_s3"]["text"])
