@@ -70,9 +70,32 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
     const BlobView B(blob);
     const uint32_t nsym = B.h->num_symbols;
     const int MAXA = rec_args(W);
-    std::string bind, csrc, build;
+    std::string bind, csrc, build, choose;
     char line[256];
     for (uint32_t f = 0; f < nsym; ++f) {
+        // rule choice of a table-planned symbol: its rules' head checks in
+        // source order (dispatch.hpp:119-130), registers against constants
+        if (B.plans[f].fast & kPlanTables) {
+            std::string body = "        case " + std::to_string(f) + ":\n";
+            for (uint32_t r = B.rule_begin[f]; r < B.rule_begin[f + 1]; ++r) {
+                const DRule& R = B.rules[r];
+                std::string cond;
+                for (uint32_t t = 0; t < R.num_steps; ++t) {
+                    const DStep& d = B.steps[R.first_step + t];
+                    if (d.kind != 0) continue;
+                    const std::string v = d.src < kSrcSlot ? "ch[" + std::to_string(d.src) + "]"
+                                                           : "gh[" + std::to_string(d.src - kSrcSlot) + "]";
+                    cond += (cond.empty() ? "" : " && ") + v + " == " + std::to_string(d.value) + "u";
+                }
+                if (cond.empty()) {
+                    body += "            return " + std::to_string(r) + ";\n";
+                    break;  // later rules are unreachable
+                }
+                body += "            if (" + cond + ") return " + std::to_string(r) + ";\n";
+            }
+            body += "            return -1;\n";
+            choose += body;
+        }
         for (uint32_t r = B.rule_begin[f]; r < B.rule_begin[f + 1]; ++r) {
             const DRule& R = B.rules[r];
             if (B.plans[f].fast & kPlanTables) {
@@ -145,6 +168,9 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
            "    const uint32_t (&ca)[kPlanChildren * 4], const uint32_t (&ga)[kPlanArgSlots * 4],\n"
            "    uint32_t (&gb)[TRS_GEN_MAXV]) {\n    switch (rule) {\n" +
            bind + "        default: break;\n    }\n}\n";
+    src += "template <int N>\n__device__ __forceinline__ int gen_choose(uint32_t sym, const uint32_t (&ch)[N],\n"
+           "    const uint32_t (&gh)[kPlanSlots]) {\n    switch (sym) {\n" +
+           choose + "        default: return -1;\n    }\n}\n";
     src += "__device__ __forceinline__ uint32_t gen_csrc(uint32_t rule, const uint32_t (&gb)[TRS_GEN_MAXV]) {\n"
            "    switch (rule) {\n" +
            csrc + "        default: return 0u;\n    }\n}\n";

@@ -252,6 +252,17 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             // first matching rule in source order (dispatch.hpp:119-130),
             // every step answered from registers
             int chosen = -1;
+#if TRS_GEN
+            if (pl.fast & kPlanTables) {
+                // specialised: the symbol's checks as compare chains against
+                // constants (first match in source order), then the bindings
+                chosen = gen_choose(sym, ch, gh);
+                if (chosen >= 0) {
+                    gen_bind<W>((uint32_t)chosen, a, ca, ga, gb);
+                    gb_ready = true;
+                }
+            } else
+#endif
             if (pl.fast & kPlanTables) {
                 // match tables: AND the rule masks of every checked position
                 // (static register reads, no walk over the rules), then bind
