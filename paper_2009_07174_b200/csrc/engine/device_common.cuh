@@ -226,6 +226,14 @@ __device__ __forceinline__ void rc_update(uint32_t* rc, int delta) {
     if (v) atomicAdd(rc, (uint32_t)v);
 }
 
+template <bool kSolo>
+__device__ __forceinline__ void rc_upd(uint32_t* rc, int delta) {
+    if (kSolo)
+        atomicAdd(rc, (uint32_t)delta);  // one lane: nothing to aggregate
+    else
+        rc_update(rc, delta);
+}
+
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x) {
     const int lane = threadIdx.x & 31;
 #pragma unroll

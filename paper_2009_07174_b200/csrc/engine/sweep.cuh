@@ -39,11 +39,23 @@ struct Slab {
 };
 
 // Mark a warp's unused slab slots dead so collections and copies skip them.
-template <int W>
+template <int W, bool kSolo = false>
 __device__ __forceinline__ void abandon_slab(uint32_t* arena, Slab& slab) {
-    const uint32_t lane = threadIdx.x & 31;
-    for (uint32_t x = slab.cur + lane; x < slab.end; x += 32) rec<W>(arena, x)[kWHead] = kDeadHead;
+    const uint32_t lane = kSolo ? 0u : (threadIdx.x & 31);
+    for (uint32_t x = slab.cur + lane; x < slab.end; x += kSolo ? 1u : 32u) rec<W>(arena, x)[kWHead] = kDeadHead;
     slab.cur = slab.end = 0;
+}
+
+// Warp collectives of the warp step, or their one-lane identities when a
+// single entry is swept by lane 0 alone (kSolo: the narrow sweeps of the
+// latency-bound configs, where the scans and ballots are pure path length).
+template <bool kSolo>
+__device__ __forceinline__ uint32_t w_scan(uint32_t x) {
+    return kSolo ? x : warp_incl_scan(x);
+}
+template <bool kSolo>
+__device__ __forceinline__ uint32_t w_bcast(uint32_t v, int src) {
+    return kSolo ? v : __shfl_sync(0xffffffffu, v, src);
 }
 
 struct StepCtx {
@@ -101,7 +113,7 @@ struct PhaseClock {
 // before its own next derive, so the next sweep skips its record gather.
 constexpr uint32_t kEntHasPayload = 1;
 
-template <int W, bool kRich>
+template <int W, bool kRich, bool kSolo = false>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
                                               Slab& slab, bool valid, const uint32_t* entry, bool prof_req,
                                               PhaseClock& pc) {
@@ -389,12 +401,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 
     // ---- claim fresh slots from the warp's slab
     const uint32_t need = act == kActBuild ? G.rules[rule].new_slots : 0;
-    const uint32_t incl = warp_incl_scan(need);
-    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t incl = w_scan<kSolo>(need);
+    const uint32_t total = w_bcast<kSolo>(incl, 31);
     uint32_t fresh = 0;
     if (total) {
         if (slab.end - slab.cur < total) {
-            abandon_slab<W>(arena, slab);
+            abandon_slab<W, kSolo>(arena, slab);
             uint32_t size = max(C.slab, total);
             uint32_t off = 0;
             if (lane == 0) {
@@ -405,8 +417,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                     off = atomicAdd(C.claim_ctr, size);
                 }
             }
-            off = __shfl_sync(0xffffffffu, off, 0);
-            size = __shfl_sync(0xffffffffu, size, 0);
+            off = w_bcast<kSolo>(off, 0);
+            size = w_bcast<kSolo>(size, 0);
             const uint64_t start = (uint64_t)C.bump + off;
             if (start + size > C.cap) {
                 // fixed capacity exhausted: the reference raises Capacity (sweep_engine.cpp:221-226)
@@ -497,7 +509,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
 #if TRS_GEN
-        gen_build<W>(rule, arena, fresh, i, ar, gb);
+        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb);
 #else
         const uint32_t nfresh = Rl.new_slots;
         for (uint32_t k = 0; k <= nfresh; ++k) {
@@ -534,7 +546,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
             for (int j = 0; j < MAXA; ++j) {
                 if ((vmask >> j) == 0u) break;
-                if ((vmask >> j) & 1u) rc_update(rec<W>(arena, b[j]) + kWRc, 1);
+                if ((vmask >> j) & 1u) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
             }
         }
 #endif
@@ -549,7 +561,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
             if ((uint32_t)j >= ar) break;
-            rc_update(rec<W>(arena, a[j]) + kWRc, -1);
+            rc_upd<kSolo>(rec<W>(arena, a[j]) + kWRc, -1);
         }
     }
     if (wword) {
@@ -578,12 +590,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     if (prof) pc.t[2] += c3 - c2;
 
     // ---- next frontier: one shared-memory reservation per warp step
-    const uint32_t pincl = warp_incl_scan(npush);
-    const uint32_t ptotal = __shfl_sync(0xffffffffu, pincl, 31);
+    const uint32_t pincl = w_scan<kSolo>(npush);
+    const uint32_t ptotal = w_bcast<kSolo>(pincl, 31);
     if (ptotal) {
         uint32_t base = 0;
         if (lane == 0) base = atomicAdd(C.push_ctr, ptotal);
-        base = __shfl_sync(0xffffffffu, base, 0);
+        base = w_bcast<kSolo>(base, 0);
         uint32_t pos = base + pincl - npush;
         if (npush) {
             if (act == kActBuild) {
@@ -639,6 +651,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         }
     }
     if (prof) pc.t[3] += clock64() - c3;
+    if (kSolo) return rewrote ? 1u : 0u;
     return __popc(__ballot_sync(0xffffffffu, rewrote));
 }
 
@@ -998,8 +1011,19 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         __syncwarp();
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
                   bind_base(P, slist)};
-        const bool valid = lane < m;
-        const uint32_t width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
+        uint32_t width;
+        if (m == 1) {
+            // one entry: lane 0 sweeps it alone, without warp collectives
+            uint32_t w1 = 0;
+            if (lane == 0) w1 = warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc * kSmallCap, prof, pc);
+            width = __shfl_sync(0xffffffffu, w1, 0);
+            // the slab is warp-uniform state: every lane takes lane 0's copy
+            slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);
+            slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
+        } else {
+            const bool valid = lane < m;
+            width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
+        }
         __syncwarp();
         L.bump += ss.claim;
         L.peak_bump = max(L.peak_bump, L.bump);
