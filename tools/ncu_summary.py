@@ -1,0 +1,56 @@
+"""Summarise the ncu captures of tools/gpu_profiles.sh into profiles/r1_ncu_summary.txt and
+profiles/traffic.json (DRAM bytes per launch, read by bench.py as roofline.traffic)."""
+import csv
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum',
+        'gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed', 'lts__t_sector_hit_rate.pct',
+        'l1tex__t_sector_hit_rate.pct', 'sm__warps_active.avg.pct_of_peak_sustained_active',
+        'smsp__issue_active.avg.pct_of_peak_sustained_active', 'launch__registers_per_thread', 'launch__grid_size',
+        'launch__block_size', 'smsp__inst_executed.sum',
+        'smsp__average_warps_issue_stalled_long_scoreboard_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_wait_per_issue_active.ratio',
+        'smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio']
+NAMES = {"fibbatch": ("config 5F fib batch, 8 shards", "fibbatch_8shards"),
+         "sortbatch": ("config 5S tree-merge-sort batch, 8 shards", "sortbatch_8shards"),
+         "buildsum22": ("config 3b build+sum depth 22", "buildsum22"),
+         "export": ("normal-form export of config 5F (trs_gpu_fetch_store)", "export_fibbatch_8shards")}
+SCALE = {'Gbyte': 1e9, 'Mbyte': 1e6, 'Kbyte': 1e3, 'byte': 1}
+
+
+def main():
+    src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
+    out = ["# Round 1 ncu summaries (specialised step loop): ncu --set full --clock-control none --import-source on",
+           "# one steady-state launch each; captured with tools/gpu_profiles.sh, summarised by tools/ncu_summary.py",
+           "#   step_loop: python tools/profile_target.py <workload>   (-k regex:step_loop -s 1 -c 1)",
+           "#   export_store: python tools/e2e_parts.py                (-k regex:export_store -c 1)",
+           "# ncu times are replayed/serialised: compare shares, not absolutes", ""]
+    traffic = {}
+    for c, (desc, key) in NAMES.items():
+        r = subprocess.run(["ncu", "-i", os.path.join(src, f"ncu_{c}.ncu-rep"), "--page", "raw", "--csv"],
+                           capture_output=True, text=True).stdout
+        rows = list(csv.reader(r.splitlines()))
+        h, u, v = rows[0], rows[1], rows[2]
+        out.append(f"## {c}: {desc}  ({v[h.index('Kernel Name')]})")
+        for w in WANT:
+            i = h.index(w)
+            out.append(f"{w:80s} {v[i]:>22s} {u[i]}")
+        rd = float(v[h.index('dram__bytes_read.sum')]) * SCALE[u[h.index('dram__bytes_read.sum')]]
+        wr = float(v[h.index('dram__bytes_write.sum')]) * SCALE[u[h.index('dram__bytes_write.sum')]]
+        out.append(f"{'dram bytes per launch (read+write)':80s} {rd + wr:22.4e} byte")
+        out.append("")
+        traffic[key] = rd + wr
+    with open(os.path.join(ROOT, "profiles", "r1_ncu_summary.txt"), "w") as f:
+        f.write("\n".join(out))
+    with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
+        json.dump(traffic, f, indent=1)
+    print("\n".join(out))
+
+
+if __name__ == "__main__":
+    main()
