@@ -117,7 +117,7 @@ typedef struct trs_gpu_options {
     uint32_t max_blocks;       /* >0: cap the persistent grid (profiling the single-CTA mode) */
     uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters); >1: only grid sweeps of <= profile entries */
     uint32_t disable_warp_mode; /* 1: frontiers <= 32 slots still run on the whole CTA */
-    uint32_t reserved[4];       /* [0] experiment flags (0); [1] bit 0: no shared-memory resident arena in
+    uint32_t reserved[4];       /* [0] zero; [1] bit 0: no shared-memory resident arena in
                                    the single-CTA mode, bit 1: interpreted (not specialised) step loop;
                                    [2] slab override (0); [3] zero */
 } trs_gpu_options;

@@ -101,7 +101,6 @@ struct Params {
     uint32_t probe_iters;   // >0: time this many grid barriers and exit (trs_gpu_overhead_probe)
     uint32_t probe_mode;
     uint32_t rich;          // grid frontier entries carry record payloads (W words) instead of bare slots
-    uint32_t debug_flags;   // experiments (trs_gpu_options.reserved[0])
     uint32_t local_cap;     // >0: slots of the shared-memory resident arena of the single-CTA mode
     uint32_t local_enter;   // allocated slots at or below which the single-CTA mode goes resident
     uint32_t max_vars;      // binding columns in shared memory (largest rule's variable count)

@@ -1191,7 +1191,6 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.fixed_capacity = opt.fixed_capacity;
     P.prefer_grow = (!opt.fixed_capacity && !opt.gc_interval && prefer_grow(e)) ? 1u : 0u;
     P.profile = opt.profile;
-    P.debug_flags = opt.reserved[0];
     P.local_cap = e->resident_on ? resident_slots(e) : 0u;
     P.local_enter = P.local_cap / 2;
     if (opt.reserved[2]) P.slab = opt.reserved[2];  // experiment: slab override

@@ -25,7 +25,6 @@ def main():
     ap.add_argument("name")
     ap.add_argument("--save", default="")
     ap.add_argument("--variant", type=int, default=0)
-    ap.add_argument("--debug-flags", type=int, default=0)
     ap.add_argument("--no-resident", action="store_true")
     ap.add_argument("--slab", type=int, default=0)
     args = ap.parse_args()
@@ -35,7 +34,6 @@ def main():
     eng = api.Engine(0)
     eng.set_program(systems[0])
     opts = api.make_options(variant=args.variant)
-    opts.reserved[0] = args.debug_flags
     opts.reserved[1] = 1 if args.no_resident else 0
     opts.reserved[2] = args.slab
     for _ in range(2):
