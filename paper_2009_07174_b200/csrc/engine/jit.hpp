@@ -18,6 +18,7 @@
 #include <nvrtc.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -162,7 +163,8 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
         }
     }
     std::string src;
-    src += "#define TRS_GEN 1\n#define TRS_GEN_MAXV " + std::to_string(max_vars) + "\n";
+    src += "#define TRS_GEN 1\n#define TRS_GEN_MAXV " + std::to_string(max_vars) + "\n#define TRS_GEN_MAXA " +
+           std::to_string(B.h->max_arity ? B.h->max_arity : 1) + "\n";
     src += "#include \"device_common.cuh\"\nnamespace trs_b200 {\n";
     src += "template <int W>\n__device__ __forceinline__ void gen_bind(uint32_t rule, const uint32_t (&a)[rec_args(W)],\n"
            "    const uint32_t (&ca)[kPlanChildren * 4], const uint32_t (&ga)[kPlanArgSlots * 4],\n"
@@ -206,9 +208,10 @@ inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", " + std::to_string(minb) + ">";
     nvrtcAddNameExpression(prog, name.c_str());
     // the specialisation is built like the library that loads it (profiling build or not)
+    const char* verbose = std::getenv("TRS_B200_JIT_VERBOSE");  // ptxas register/spill report in the log
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                          TRS_B200_PROFILE ? "-DTRS_B200_PROFILE=1" : "-DTRS_B200_PROFILE=0"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, 4, opts);
+                          TRS_B200_PROFILE ? "-DTRS_B200_PROFILE=1" : "-DTRS_B200_PROFILE=0", "--ptxas-options=-v"};
+    const nvrtcResult rc = nvrtcCompileProgram(prog, (verbose && verbose[0] == '1') ? 5 : 4, opts);
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
     out.log.resize(n);

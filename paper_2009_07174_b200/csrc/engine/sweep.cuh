@@ -119,6 +119,13 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                                               PhaseClock& pc) {
     const bool prof = kProfBuild && prof_req;
     constexpr int MAXA = rec_args(W);
+    // arguments any symbol of the program has: the specialisation knows it,
+    // so loops over arguments stop there and their registers disappear
+#if TRS_GEN
+    constexpr int AE = TRS_GEN_MAXA < MAXA ? TRS_GEN_MAXA : MAXA;
+#else
+    constexpr int AE = MAXA;
+#endif
     const uint32_t s = C.s;
     const uint32_t lane = threadIdx.x & 31;
     long long c0 = prof ? clock64() : 0;
@@ -204,6 +211,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         for (int j = 0; j < MAXA; ++j) {
             ch[j] = 0;
             cep[j] = 1;
+        }
+#pragma unroll
+        for (int j = 0; j < (int)kPlanChildren * 4; ++j) ca[j] = 0;
+#pragma unroll
+        for (int j = 0; j < AE; ++j) {
             if ((uint32_t)j < ar) {
                 const uint32_t* C = rec<W>(arena, a[j]);
                 if (j < (int)kPlanChildren && ((pl.child_args >> j) & 1u)) {
@@ -221,13 +233,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                     cep[j] = c.y;
                 }
             }
-            if (j < (int)kPlanChildren && !((uint32_t)j < ar && ((pl.child_args >> j) & 1u)))
-                ca[j * 4 + 0] = ca[j * 4 + 1] = ca[j * 4 + 2] = ca[j * 4 + 3] = 0;
         }
         if (prof) pc.mark(1, cep[0] ^ cep[MAXA - 1] ^ ca[0]);
         bool pending = false;
 #pragma unroll
-        for (int j = MAXA - 1; j >= 0; --j) {
+        for (int j = AE - 1; j >= 0; --j) {
             // nf_read(c) at sweep s: nf since an earlier sweep (sweep_engine.cpp:80-81)
             if ((uint32_t)j >= cursor && (uint32_t)j < ar && (cep[j] == 0 || cep[j] >= s)) {
                 pending = true;
@@ -283,7 +293,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 const uint32_t nr = G.rule_begin[sym + 1] - G.rule_begin[sym];
                 uint32_t mask = nr >= 32 ? 0xFFFFFFFFu : (1u << nr) - 1u;
 #pragma unroll
-                for (int q = 0; q < MAXA; ++q) {
+                for (int q = 0; q < AE; ++q) {
                     const uint16_t row = rows[q];
                     if (row != kNoRow) mask &= G.mtab[row + ch[q]];
                 }
@@ -520,7 +530,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
             for (int j = 0; j < MAXA; ++j) b[j] = 0;
 #pragma unroll
-            for (int j = 0; j < MAXA; ++j) {
+            for (int j = 0; j < AE; ++j) {
                 if ((uint32_t)j >= iar) break;
                 const uint16_t ref = G.refs[I.first_ref + j];
                 const bool var = !(ref & kRefNode);
@@ -544,7 +554,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             }
             // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
 #pragma unroll
-            for (int j = 0; j < MAXA; ++j) {
+            for (int j = 0; j < AE; ++j) {
                 if ((vmask >> j) == 0u) break;
                 if ((vmask >> j) & 1u) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
             }
@@ -559,7 +569,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // the reference orders them; sweep_engine.cpp:255-256)
     if (rewrote) {
 #pragma unroll
-        for (int j = 0; j < MAXA; ++j) {
+        for (int j = 0; j < AE; ++j) {
             if ((uint32_t)j >= ar) break;
             rc_upd<kSolo>(rec<W>(arena, a[j]) + kWRc, -1);
         }
