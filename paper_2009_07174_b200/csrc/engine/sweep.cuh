@@ -1022,9 +1022,9 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
                   bind_base(P, slist)};
         uint32_t width;
-        // (the wide-record variants skip the solo path: another inlined
-        // warp step costs them spills that the wide sweeps pay for)
-        if (W == 8 && m == 1) {
+        // (the interpreted wide-record variants skip the solo path: another
+        // inlined warp step costs them spills that the wide sweeps pay for)
+        if ((W == 8 || TRS_GEN) && m == 1) {
             // one entry: lane 0 sweeps it alone, without warp collectives
             uint32_t w1 = 0;
             if (lane == 0) w1 = warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc * kSmallCap, prof, pc);
