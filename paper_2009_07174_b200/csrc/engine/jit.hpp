@@ -107,6 +107,25 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
                     std::snprintf(line, sizeof line, " gb[%u] = %s;", d.value, jit_src_expr(d.src).c_str());
                     body += line;
                 }
+                if (R.collapse && R.csrc != kNone) {
+                    // the collapse source's record, already in registers
+                    const unsigned cs = R.csrc;
+                    if (cs < kSrcSlot) {
+                        std::snprintf(line, sizeof line, " cs_head = ch[%u];", cs);
+                        body += line;
+                        for (int k = 0; k < 4; ++k) {
+                            std::snprintf(line, sizeof line, " cs_b[%d] = ca[%u];", k, (cs & 3u) * 4 + k);
+                            body += line;
+                        }
+                    } else {
+                        std::snprintf(line, sizeof line, " cs_head = gh[%u];", cs & 3u);
+                        body += line;
+                        for (int k = 0; k < 4; ++k) {
+                            std::snprintf(line, sizeof line, " cs_b[%d] = ga[%u];", k, (cs & 1u) * 4 + k);
+                            body += line;
+                        }
+                    }
+                }
                 if (!body.empty()) bind += "        case " + std::to_string(r) + ":" + body + " break;\n";
             }
             if (R.collapse) {
@@ -163,12 +182,17 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
         }
     }
     std::string src;
+    bool all_tables = true;  // every symbol with rules chooses by tables: the rule walks compile out
+    for (uint32_t f = 0; f < nsym; ++f)
+        if (B.rule_begin[f + 1] > B.rule_begin[f] && !(B.plans[f].fast & kPlanTables)) all_tables = false;
     src += "#define TRS_GEN 1\n#define TRS_GEN_MAXV " + std::to_string(max_vars) + "\n#define TRS_GEN_MAXA " +
-           std::to_string(B.h->max_arity ? B.h->max_arity : 1) + "\n";
+           std::to_string(B.h->max_arity ? B.h->max_arity : 1) + "\n#define TRS_GEN_ALL_TABLES " +
+           (all_tables ? "1" : "0") + "\n";
     src += "#include \"device_common.cuh\"\nnamespace trs_b200 {\n";
     src += "template <int W>\n__device__ __forceinline__ void gen_bind(uint32_t rule, const uint32_t (&a)[rec_args(W)],\n"
-           "    const uint32_t (&ca)[kPlanChildren * 4], const uint32_t (&ga)[kPlanArgSlots * 4],\n"
-           "    uint32_t (&gb)[TRS_GEN_MAXV]) {\n    switch (rule) {\n" +
+           "    const uint32_t (&ch)[rec_args(W)], const uint32_t (&ca)[kPlanChildren * 4],\n"
+           "    const uint32_t (&gh)[kPlanSlots], const uint32_t (&ga)[kPlanArgSlots * 4],\n"
+           "    uint32_t (&gb)[TRS_GEN_MAXV], uint32_t& cs_head, uint32_t (&cs_b)[4]) {\n    switch (rule) {\n" +
            bind + "        default: break;\n    }\n}\n";
     src += "template <int N>\n__device__ __forceinline__ int gen_choose(uint32_t sym, const uint32_t (&ch)[N],\n"
            "    const uint32_t (&gh)[kPlanSlots]) {\n    switch (sym) {\n" +

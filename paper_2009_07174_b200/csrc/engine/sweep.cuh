@@ -80,6 +80,9 @@ constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
 #ifndef TRS_GEN
 #define TRS_GEN 0
 #endif
+#ifndef TRS_GEN_ALL_TABLES
+#define TRS_GEN_ALL_TABLES 0
+#endif
 // The rich frontier-entry format (record payloads in the list) is compiled
 // only on request (-DTRS_B200_RICH_ENTRIES=1): its extra inlined copy of the
 // warp step doubles the grid sweep's code for an opt-in format.
@@ -280,10 +283,17 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 // constants (first match in source order), then the bindings
                 chosen = gen_choose(sym, ch, gh);
                 if (chosen >= 0) {
-                    gen_bind<W>((uint32_t)chosen, a, ca, ga, gb);
+                    gen_bind<W>((uint32_t)chosen, a, ch, ca, gh, ga, gb, cs_head, cs_b);
                     gb_ready = true;
                 }
-            } else
+            }
+#endif
+#if TRS_GEN && TRS_GEN_ALL_TABLES
+            // every symbol with rules has match tables: the walks below are
+            // unreachable (a planned symbol without tables has no rules)
+#else
+#if TRS_GEN
+            else
 #endif
             if (pl.fast & kPlanTables) {
                 // match tables: AND the rule masks of every checked position
@@ -345,13 +355,18 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                     }
                 }
             }
+#endif
             if (chosen < 0) {
                 act = kActNf;
             } else {
                 rule = (uint32_t)chosen;
                 const DRule& Rl = G.rules[rule];
                 act = Rl.collapse ? kActCollapse : kActBuild;
+#if TRS_GEN
+                if (!gb_ready && Rl.collapse && Rl.csrc != kNone) {  // gen_bind set them on the table path
+#else
                 if (Rl.collapse && Rl.csrc != kNone) {
+#endif
                     const uint32_t cs = Rl.csrc;
                     cs_head = cs < kSrcSlot ? pick(ch, cs) : pick(gh, cs & 3u);
 #pragma unroll
@@ -360,6 +375,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 }
             }
         } else {
+#if TRS_GEN && TRS_GEN_ALL_TABLES
+            act = kActNf;  // unreachable: every symbol is planned
+#else
             // interpreted matcher: one dependent gather per step below the root
             uint32_t stepnode[kMaxRuleSteps];
             int chosen = -1;
@@ -397,9 +415,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 rule = (uint32_t)chosen;
                 act = G.rules[rule].collapse ? kActCollapse : kActBuild;
             }
+#endif
         }
     }
-#if TRS_GEN
+#if TRS_GEN && !TRS_GEN_ALL_TABLES
     if (!gb_ready && (act == kActCollapse || act == kActBuild)) {
 #pragma unroll
         for (int v = 0; v < TRS_GEN_MAXV; ++v) gb[v] = TRS_BIND(v);
