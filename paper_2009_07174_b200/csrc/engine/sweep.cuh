@@ -1022,16 +1022,70 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
     const uint32_t lane = threadIdx.x & 31;
     PhaseClock pc;
     const bool prof = kProfBuild && P.profile == 1 && lane == 0;
+    uint64_t t_prev = global_ns();  // one timer read per sweep: each sweep's ns runs from the previous one's end
     for (;;) {
         const uint32_t sc = ss.sc;
         const uint32_t m = ss.count[sc];
         if (m == 0 || m > 32) break;
+        if (W == 8 && m == 1) {
+            // Solo sweeps: while the frontier is a single slot, lane 0 runs
+            // sweep after sweep alone -- the warp step without collectives and
+            // the loop's bookkeeping without warp synchronisation -- and hands
+            // its state to the warp when the frontier widens or the run stops.
+            // (Wide-record kernels take the one-sweep solo step below instead:
+            // this loop's extra state costs them spills.)
+            if (lane == 0) {
+                for (;;) {
+                    const uint32_t sc1 = ss.sc;
+                    if (ss.count[sc1] != 1) break;
+                    if (slab_size == 0 && (uint64_t)L.bump + P.max_new + 1 > cap) break;
+                    if (plan(P, L, 1, just_collected, 1) != kPlanSweep) break;
+                    just_collected = false;
+                    const uint32_t s = L.sweep + 1;
+                    const long long cs = prof ? clock64() : 0;
+                    ss.count[sc1 ^ 1] = 0;
+                    ss.claim = 0;
+                    StepCtx C{s, L.bump, &ss.claim, slist + (sc1 ^ 1) * kSmallCap, &ss.count[sc1 ^ 1], &ss.abort,
+                              cap, slab_size, bind_base(P, slist)};
+                    const uint32_t width =
+                        warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc1 * kSmallCap, prof, pc);
+                    L.bump += ss.claim;
+                    L.peak_bump = max(L.peak_bump, L.bump);
+                    L.total += width;
+                    L.maxw = width > L.maxw ? width : L.maxw;
+                    L.sweep = s;
+                    L.small_sweeps++;
+                    ss.sc = sc1 ^ 1;
+                    const uint64_t now = global_ns();
+                    record(P, s, width, L, 1, 2, now - t_prev);
+                    t_prev = now;
+                    if (prof) {
+                        for (int k = 0; k < 4; ++k) P.ctl->prof[k] += pc.t[k];
+                        P.ctl->prof[4] += clock64() - cs;
+                        P.ctl->prof[5] += 1;
+                        P.ctl->prof[6] += pc.steps;
+                        pc = PhaseClock{};
+                    }
+                    if (L.total > P.step_budget || ss.abort) break;
+                }
+                ss.L = L;
+            }
+            __syncwarp();
+            L = ss.L;
+            just_collected = false;
+            t_prev = __shfl_sync(0xffffffffu, t_prev, 0);
+            slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);
+            slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
+            __syncwarp();
+            if (L.total > P.step_budget || ss.abort) break;
+            if (ss.count[ss.sc] == 1) break;  // stopped by plan or headroom: the caller decides
+            continue;
+        }
         // a resident arena must hold the worst case of this sweep
         if (slab_size == 0 && (uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap) break;
         if (plan(P, L, m, just_collected, 1) != kPlanSweep) break;
         just_collected = false;
         const uint32_t s = L.sweep + 1;
-        const uint64_t t0 = global_ns();
         const long long cs = prof ? clock64() : 0;
         if (lane == 0) {
             ss.count[sc ^ 1] = 0;
@@ -1041,15 +1095,12 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
                   bind_base(P, slist)};
         uint32_t width;
-        // (the interpreted wide-record variants skip the solo path: another
-        // inlined warp step costs them spills that the wide sweeps pay for)
-        if ((W == 8 || TRS_GEN) && m == 1) {
-            // one entry: lane 0 sweeps it alone, without warp collectives
+        if (TRS_GEN && W != 8 && m == 1) {
+            // one entry, specialised wide-record kernel: lane 0 alone for this sweep
             uint32_t w1 = 0;
             if (lane == 0) w1 = warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc * kSmallCap, prof, pc);
             width = __shfl_sync(0xffffffffu, w1, 0);
-            // the slab is warp-uniform state: every lane takes lane 0's copy
-            slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);
+            slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);  // the slab is warp-uniform state
             slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
         } else {
             const bool valid = lane < m;
@@ -1062,9 +1113,10 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         L.maxw = width > L.maxw ? width : L.maxw;
         L.sweep = s;
         L.small_sweeps++;
+        const uint64_t now = global_ns();
         if (lane == 0) {
             ss.sc = sc ^ 1;
-            record(P, s, width, L, m, 2, global_ns() - t0);
+            record(P, s, width, L, m, 2, now - t_prev);
             if (prof) {
                 for (int k = 0; k < 4; ++k) P.ctl->prof[k] += pc.t[k];
                 P.ctl->prof[4] += clock64() - cs;
@@ -1073,6 +1125,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                 pc = PhaseClock{};
             }
         }
+        t_prev = now;
         __syncwarp();
         if (L.total > P.step_budget || ss.abort) break;
     }
