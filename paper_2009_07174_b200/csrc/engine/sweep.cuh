@@ -1,8 +1,11 @@
 // The step loop: one persistent cooperative launch runs every sweep.
 //
 // A sweep (the reference's derive_phase + fold, sweep_engine.cpp:69-188)
-// processes the awake frontier in 32-entry chunks, one entry per lane, with
-// warps running independently: no CTA-wide barrier inside a sweep.
+// processes the awake frontier in chunks of q <= 32 entries, one entry per
+// lane, with warps running independently: no CTA-wide barrier inside a sweep.
+//  * Derive: record, children and (planned) grandchildren loaded level by
+//    level; the rule chosen by match tables, or by generated compare chains
+//    in the per-program specialisation (TRS_GEN, jit.hpp).
 //  * Fresh slots come from per-warp slabs (one atomic per slab, not per
 //    rewrite; get_new_index, term_store.cpp:118-138).
 //  * Next-frontier pushes go to the CTA's own region of the output list,
@@ -10,8 +13,10 @@
 //    region table (offset, count, rewrites) is read back after the grid
 //    barrier, so a sweep has no contended global atomics at all.
 //  * Tiny frontiers run on CTA 0 alone out of shared memory (single-CTA
-//    mode), and frontiers of <= 32 slots on one warp of it (warp mode),
-//    with __syncthreads / __syncwarp instead of the grid barrier.
+//    mode), frontiers of <= 32 slots on one warp of it (warp mode), a single
+//    slot on one lane (solo), with __syncthreads / __syncwarp / nothing
+//    instead of the grid barrier; small stores move into shared memory
+//    altogether (the resident arena).
 #pragma once
 
 #include "gc.cuh"
