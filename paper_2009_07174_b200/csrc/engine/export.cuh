@@ -42,14 +42,36 @@ template <int W>
 __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X, uint32_t bump) {
     __shared__ Smem sm;
     const uint32_t* A = P.arena[__ldcg(&P.ctl->arena)];
-    const uint8_t* arity = P.prog + reinterpret_cast<const ProgHeader*>(P.prog)->off_arity;  // global copy
+    // symbol arities in shared memory when they fit (a chain walk reads one per hop)
+    __shared__ uint8_t s_arity[4096];
+    const ProgHeader* ph = reinterpret_cast<const ProgHeader*>(P.prog);
+    const uint8_t* g_arity = P.prog + ph->off_arity;
+    const bool arity_in_smem = ph->num_symbols <= 4096;
+    if (arity_in_smem)
+        for (uint32_t f = threadIdx.x; f < ph->num_symbols; f += kBlock) s_arity[f] = g_arity[f];
+    __syncthreads();
+    const uint8_t* arity = arity_in_smem ? s_arity : g_arity;
     const uint32_t nblocks = gridDim.x;
     const uint32_t tid = blockIdx.x * kBlock + threadIdx.x;
     const uint32_t nthreads = nblocks * kBlock;
     uint32_t epoch = 0;
+#if TRS_B200_PROFILE
+    // profiling build: phase ns (clear, mark, renumber, pack) in ctl->gcprof
+    const bool gl = blockIdx.x == 0 && threadIdx.x == 0;
+    uint64_t gt = gl ? global_ns() : 0;
+#define TRS_EXPORT_MARK(k)                       \
+    if (gl) {                                    \
+        const uint64_t now = global_ns();        \
+        P.ctl->gcprof[k] = now - gt;             \
+        gt = now;                                \
+    }
+#else
+#define TRS_EXPORT_MARK(k)
+#endif
     // clear the reference counters
     for (uint32_t y = tid; y < bump; y += nthreads) X.newrc[y] = 0;
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_EXPORT_MARK(0)
     // Marking runs on one shared work queue with no levels: an S^k numeral
     // under a deep tree would otherwise cost a whole chain walk per level.
     // Items are pushed by a tail counter into zeroed slots; a thread claims
@@ -106,13 +128,18 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         red_release_add(pending, 0xFFFFFFFFu);  // -1, ordered after this item's pushes
     }
     grid_sync(P.ctl, nblocks, epoch);
+    TRS_EXPORT_MARK(1)
     // renumber live slots in arena order: per-CTA contiguous ranges
     const uint32_t span = bump - 1;
     const uint32_t chunk = (span + nblocks - 1) / nblocks;
     const uint32_t lo = 1 + blockIdx.x * chunk;
     const uint32_t hi = min(bump, lo + chunk);
+    constexpr uint32_t kPer = 8;  // slots per thread per pass: their loads issue together
     uint32_t cnt = 0;
-    for (uint32_t y = lo + threadIdx.x; y < hi; y += kBlock) cnt += __ldcg(X.newrc + y) != 0u;
+    for (uint32_t y0 = lo + threadIdx.x * kPer; y0 < hi; y0 += kBlock * kPer) {
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) cnt += (y0 + k < hi && __ldcg(X.newrc + y0 + k) != 0u) ? 1u : 0u;
+    }
     uint32_t tot;
     block_scan(cnt, &tot, sm);
     if (threadIdx.x == 0) P.blocksum[blockIdx.x] = tot;
@@ -130,13 +157,21 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         prefix = t1;
         all = t2;
     }
+    // eight consecutive slots per thread: one block scan per 4096 slots
     uint32_t running = 1 + prefix;
-    for (uint32_t y0 = lo; y0 < hi; y0 += kBlock) {
-        const uint32_t y = y0 + threadIdx.x;
-        const bool live = y < hi && __ldcg(X.newrc + y) != 0u;
+    for (uint32_t y0 = lo; y0 < hi; y0 += kBlock * kPer) {
+        const uint32_t yb = y0 + threadIdx.x * kPer;
+        uint32_t live = 0;  // bit k: slot yb + k is live
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k)
+            if (yb + k < hi && __ldcg(X.newrc + yb + k) != 0u) live |= 1u << k;
         uint32_t t;
-        const uint32_t e = block_scan(live ? 1u : 0u, &t, sm);
-        if (y < hi) X.map[y] = live ? running + e : 0u;
+        uint32_t e = running + block_scan(__popc(live), &t, sm);
+#pragma unroll
+        for (uint32_t k = 0; k < kPer; ++k) {
+            if (yb + k < hi) X.map[yb + k] = ((live >> k) & 1u) ? e : 0u;
+            e += (live >> k) & 1u;
+        }
         running += t;
     }
     const uint32_t n = 1 + all;
@@ -145,9 +180,17 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         X.map[0] = 0;
     }
     grid_sync(P.ctl, nblocks, epoch);
-    // pack the columns
-    for (uint32_t y = 1 + tid; y < bump; y += nthreads) {
-        const uint32_t rc = __ldcg(X.newrc + y);
+    TRS_EXPORT_MARK(2)
+    // pack the columns: eight slots per thread per pass, their reference
+    // counts loaded together (most slots are garbage and only cost that load)
+    for (uint32_t y0 = 1 + tid * kPer; y0 < bump; y0 += nthreads * kPer) {
+        uint32_t rcs[kPer];
+#pragma unroll
+        for (uint32_t q = 0; q < kPer; ++q) rcs[q] = y0 + q < bump ? __ldcg(X.newrc + y0 + q) : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < kPer; ++q) {
+        const uint32_t y = y0 + q;
+        const uint32_t rc = rcs[q];
         if (!rc) continue;
         const uint32_t k = __ldcg(X.map + y);
         const uint32_t* R = A + (size_t)y * W;
@@ -159,6 +202,7 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         X.nf[k] = q0.y != 0;
         for (uint32_t j = 0; j < X.ma; ++j)
             X.args[(size_t)j * n + k] = j < ar ? __ldcg(X.map + __ldcg(R + kWArgs + j)) : 0u;
+        }
     }
     if (tid == 0) {
         X.hss[0] = 0;
@@ -167,6 +211,10 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         for (uint32_t j = 0; j < X.ma; ++j) X.args[(size_t)j * n] = 0;
     }
     for (uint32_t r = tid; r < P.num_roots; r += nthreads) X.roots_out[r] = __ldcg(X.map + P.roots[r]);
+#if TRS_B200_PROFILE
+    grid_sync(P.ctl, nblocks, epoch);
+    TRS_EXPORT_MARK(3)
+#endif
 }
 
 }  // namespace trs_b200
