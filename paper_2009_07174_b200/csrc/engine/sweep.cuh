@@ -110,16 +110,18 @@ struct PhaseClock {
     }
 };
 
-// One entry per lane: derive (sweep_engine.cpp:163-188), claim, apply
-// (:190-258), push.  Every lane of the warp must call it (valid or not).
-// Returns the warp's number of rewrites.
-// Frontier entries.  Single-CTA lists hold bare slot ids.  Grid lists
-// ("rich" entries) hold W words laid out like a record,
+// Frontier entries are bare slot ids.  The opt-in rich format
+// (TRS_B200_RICH_ENTRIES) holds W words laid out like a record,
 //   [slot, head|cursor, has_payload, 0, args...],
 // where the pusher copies the node's head and arguments whenever it knows
 // them (fresh nodes, rewritten roots, polls): the node cannot change
 // before its own next derive, so the next sweep skips its record gather.
 constexpr uint32_t kEntHasPayload = 1;
+
+// One entry per lane: derive (sweep_engine.cpp:163-188), claim, apply
+// (:190-258), push.  Every lane of the warp must call it (valid or not),
+// except in the solo form (kSolo), which lane 0 runs alone for a one-entry
+// sweep.  Returns the warp's number of rewrites.
 
 template <int W, bool kRich, bool kSolo = false>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
