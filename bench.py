@@ -438,6 +438,9 @@ def main():
 
     hbm_peak, peak_kind = measured_peaks()
     gather_gbps = api.gather_probe(local, 4 << 30, 4, 5)
+    # the same probe at 8/16/32 bytes per access: the random-access rate is
+    # the limit (flat up to 16 B), not bytes
+    gather_wide = {f"{b}B_gbps": api.gather_probe(local, 4 << 30, b, 3) for b in (8, 16, 32)}
     kernel_ms = statistics.mean(s["kernel_ms"] for s in stats)
     roofline = None
     if all(fx):
@@ -460,7 +463,9 @@ def main():
             "gather": {"achieved_gbps": 4 * A / t / 1e9, "roofline_gbps": gather_gbps,
                        "frac": 4 * A / t / 1e9 / gather_gbps,
                        "definition": "4 B x A / step-loop time vs measured uniformly random 4-B gather over "
-                                     "4 GiB (trs_gpu_gather_probe)"},
+                                     "4 GiB (trs_gpu_gather_probe)",
+                       "accesses_per_s": A / t, "roofline_accesses_per_s": gather_gbps * 1e9 / 4,
+                       "probe_wider": gather_wide},
             "t_roof_frac": max(4 * A / (gather_gbps * 1e9), smin / (hbm_peak * 1e9)) / t,
         }
     cpu = None
