@@ -105,11 +105,22 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
             if (ns < 1024) ns <<= 1;
         }
         if (x == 0u) break;
+        uint4 h4 = make_uint4(0u, 0u, 0u, 0u), a4 = h4;
+        if (x) {
+            h4 = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)x * W));
+            a4 = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)x * W + kWArgs));
+        }
         while (x) {
             const uint32_t* R = A + (size_t)x * W;
-            const uint4 h4 = __ldcg(reinterpret_cast<const uint4*>(R));
-            const uint4 a4 = __ldcg(reinterpret_cast<const uint4*>(R + kWArgs));
             const uint32_t ar = arity[h4.x & kSymMask];
+            // speculate that the walk continues into the first argument (S^k
+            // numerals, list spines): its record load overlaps the reference
+            // count round trip that decides it
+            uint4 sh = make_uint4(0u, 0u, 0u, 0u), sa = sh;
+            if (ar) {
+                sh = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)a4.x * W));
+                sa = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)a4.x * W + kWArgs));
+            }
             uint32_t next = 0;
             for (uint32_t j = 0; j < ar; ++j) {
                 const uint32_t c = j == 0 ? a4.x : j == 1 ? a4.y : j == 2 ? a4.z : j == 3 ? a4.w : __ldcg(R + kWArgs + j);
@@ -122,6 +133,13 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
                         asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(Q + t), "r"(c) : "memory");
                     }
                 }
+            }
+            if (next && next == a4.x) {
+                h4 = sh;
+                a4 = sa;
+            } else if (next) {
+                h4 = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)next * W));
+                a4 = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)next * W + kWArgs));
             }
             x = next;
         }
