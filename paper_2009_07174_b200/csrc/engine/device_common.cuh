@@ -197,11 +197,12 @@ __device__ __forceinline__ unsigned long long block_sum64(unsigned long long v, 
     for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
     if (lane == 0) sm.red[warp] = v;
     __syncthreads();
-    // every thread reduces the warp sums with shuffles: 4 steps instead of a
-    // 16-iteration shared-memory loop
+    // every thread reduces the warp sums with a full 32-lane butterfly
+    // (lanes >= kWarps hold zero), so every lane of the block gets the total:
+    // the single-CTA loop keeps per-thread counters from it and breaks on them
     unsigned long long t = lane < kWarps ? sm.red[lane] : 0ull;
 #pragma unroll
-    for (int o = kWarps / 2; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
     __syncthreads();
     return t;
 }

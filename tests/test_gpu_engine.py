@@ -330,3 +330,64 @@ def test_async_run_behind_stream_gate(engine):
     np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
     with pytest.raises(ValueError):
         engine.run_wait()  # nothing pending
+
+
+def test_export_after_step_budget(engine):
+    """A run stopped by the step budget leaves a partial store; the export
+    still writes back a consistent one (every slot reachable, refcounts =
+    references from exported slots + root pins) with non-normal subterms."""
+    g = CASES["fib12"]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    v = st.view()
+    engine.set_program(s)
+    engine.load(st)
+    with pytest.raises(api.EngineError) as ei:
+        engine.run(api.make_options(step_budget=100))
+    assert ei.value.fault == api.EngineFault.StepBudget
+    out = engine.fetch_store(v["maxarity"], v["num_roots"])
+    n = out["n"]
+    counted = np.zeros(n, np.int64)
+    for r in out["roots"]:
+        counted[r] += 1
+    for y in range(1, n):
+        for j in range(s.symbol_arity(int(out["hss"][y]))):
+            c = out["args"][j, y]
+            assert 0 < c < n
+            counted[c] += 1
+    np.testing.assert_array_equal(out["refcounts"][1:], counted[1:])
+    assert (counted[1:] > 0).all()
+    assert not out["nf"][1:].all()  # stopped before the normal form
+
+
+@pytest.mark.parametrize("mode", ["default", "no_warp", "no_resident", "interp", "grid_only"])
+@pytest.mark.parametrize("budget", [1, 10, 100, 1000])
+def test_step_budget_every_mode(engine, mode, budget):
+    """The budget stop is uniform in every execution mode: whichever mode the
+    run is in when the total passes the budget (warp, single-CTA, resident,
+    grid), the launch ends with StepBudget and the stats report the total."""
+    g = CASES["fib12"]
+    o = api.make_options(step_budget=budget)
+    if mode == "no_warp":
+        o.disable_warp_mode = 1
+    if mode == "no_resident":
+        o.reserved[1] = 1
+    if mode == "interp":
+        o.reserved[1] = 2
+    if mode == "grid_only":
+        o.disable_small = 1
+    assert g["rewrites"] > budget
+    with pytest.raises(api.EngineError) as ei:
+        api.normalize_texts(g["text"], engine=engine, options=o)
+    assert ei.value.fault == api.EngineFault.StepBudget
+
+
+@pytest.mark.parametrize("name", ["ackermann23", "fib12", "mergesort50_s42", "reverse64", "unit_two_waiters"])
+def test_no_warp_mode_is_invisible(engine, name):
+    """Without the one-warp mode tiny frontiers run on the whole CTA: same
+    widths, rewrites and normal form."""
+    g = CASES[name]
+    res = run(engine, g["text"], disable_warp_mode=1)
+    assert res.total_rewrites == g["rewrites"]
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
