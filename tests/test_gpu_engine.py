@@ -117,7 +117,9 @@ def _pad_add(a, b):
 
 
 @pytest.mark.parametrize("opts", [dict(variant=2), dict(max_blocks=1), dict(small_enter=1 << 20, small_exit=1 << 20),
-                                  dict(disable_small=1, gc_interval=3), dict(blocks_per_sm=1, small_enter=4)])
+                                  dict(disable_small=1, gc_interval=3), dict(blocks_per_sm=1, small_enter=4),
+                                  dict(profile=1), dict(disable_warp_mode=1, max_blocks=3), dict(disable_gc=1),
+                                  dict(small_enter=40, small_exit=40), dict(validate=1, gc_interval=1)])
 @pytest.mark.parametrize("name", ["treemergesort_4_5_s7", "fibbatch64_s3", "unit_two_waiters", "transform6"])
 def test_knobs_do_not_change_results(engine, name, opts):
     g = CASES[name]
@@ -388,6 +390,20 @@ def test_no_warp_mode_is_invisible(engine, name):
     widths, rewrites and normal form."""
     g = CASES[name]
     res = run(engine, g["text"], disable_warp_mode=1)
+    assert res.total_rewrites == g["rewrites"]
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+
+
+@pytest.mark.parametrize("slab", [1, 7, 64, 4096])
+@pytest.mark.parametrize("name", ["treemergesort_4_5_s7", "fibbatch64_s3", "unit_two_waiters"])
+def test_slab_size_does_not_change_results(engine, name, slab):
+    """The per-warp slab of fresh slots (allocator granularity, including
+    slabs smaller than one rewrite's template) changes slot numbering only."""
+    g = CASES[name]
+    o = api.make_options(validate=1)
+    o.reserved[2] = slab
+    res = api.normalize_texts(g["text"], engine=engine, options=o)
     assert res.total_rewrites == g["rewrites"]
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
     np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
