@@ -60,10 +60,10 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
 #define TRS_GC_MARK(k)
 #endif
     // phase 1: claim refcount-zero slots and drop their argument references.
-    // A thread follows the cascade it triggers for at most max_hops hops (64
-    // inside the step loop, bounding the pause; unbounded for the final
-    // compaction); the rest waits for a later collection, as the reference
-    // defers it.
+    // A thread follows the cascade it triggers for at most max_hops claimed
+    // slots (64 inside the step loop, bounding the pause; unbounded for the
+    // final compaction); the rest waits for a later collection, as the
+    // reference defers it.
     for (uint32_t x = 1 + tid; x < bump; x += nthreads) {
         uint32_t* R = rec<W>(A, x);
         const uint4 hq = __ldcg(reinterpret_cast<const uint4*>(R));  // head, epoch, rc, waiter
@@ -71,18 +71,23 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
         if (head == kDeadHead || hq.z != 0) continue;
         if (atomicCAS(R + kWHead, head, kDeadHead) != head) continue;
         uint32_t cur_slot = x, chead = head;
-        for (int hop = 0;; ++hop) {
-            if ((uint32_t)hop == max_hops) {
-                // cascade cut short: the next collection finishes it
-                P.ctl->gc_truncated = 1u;
-                break;
-            }
+        for (uint32_t hop = 0;; ++hop) {
+            // a claimed slot always drops its references; at the hop cap the
+            // children it frees stay unclaimed with refcount zero (live to
+            // the compaction), and the next collection's scan takes them
+            const bool last = hop + 1 >= max_hops;
             uint32_t* C = rec<W>(A, cur_slot);
             uint32_t car = G.arity[chead & kSymMask];
             uint32_t next = 0, nhead = 0;
             for (uint32_t j = 0; j < car; ++j) {
                 uint32_t c = __ldcg(C + kWArgs + j);
-                if (atomicSub(rec<W>(A, c) + kWRc, 1u) == 1u && next == 0) {
+                const bool freed = atomicSub(rec<W>(A, c) + kWRc, 1u) == 1u;
+                if (!freed) continue;
+                if (last || next != 0) {
+                    // not followed (hop cap, or a second freed child): it stays
+                    // garbage unless this pass's scan reaches it later
+                    P.ctl->gc_truncated = 1u;
+                } else {
                     uint32_t h = __ldcg(rec<W>(A, c) + kWHead);
                     if (h != kDeadHead && atomicCAS(rec<W>(A, c) + kWHead, h, kDeadHead) == h) {
                         next = c;
@@ -92,7 +97,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
             }
 #if TRS_B200_PROFILE
             hops_total++;
-            hops_max = max(hops_max, (uint32_t)hop + 1);
+            hops_max = max(hops_max, hop + 1);
 #endif
             if (!next) break;
             cur_slot = next;

@@ -158,7 +158,8 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
                                   "              *reinterpret_cast<uint4*>(F) = make_uint4(%uu, 0u, %uu, %s);\n",
                                   k, I.symbol | ((uint32_t)I.cursor << kSymBits), (unsigned)I.indegree, sub.c_str());
                     body += line;
-                    for (uint32_t q = 0; q * 4 < iar; ++q)
+                    // the first argument quad always (zeros past the arity: sweep.cuh's build)
+                    for (uint32_t q = 0; q == 0 || q * 4 < iar; ++q)
                         body += "              *reinterpret_cast<uint4*>(F + kWArgs + " + std::to_string(q * 4) +
                                 ") = make_uint4(" + args[q * 4] + ", " + args[q * 4 + 1] + ", " + args[q * 4 + 2] +
                                 ", " + args[q * 4 + 3] + ");\n";

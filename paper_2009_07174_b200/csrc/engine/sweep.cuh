@@ -567,10 +567,15 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 uint32_t sub = I.subscriber == kNone ? 0u : I.subscriber == kRootSub ? i : fresh + I.subscriber;
                 uint32_t* F = rec<W>(arena, fresh + k);
                 *reinterpret_cast<uint4*>(F) = make_uint4(I.symbol | ((uint32_t)I.cursor << kSymBits), 0u, I.indegree, sub);
-                // argument quads past the arity are never read: leave them unwritten
+                // argument quads past the arity are never read, except the
+                // first: a planned match loads a child's first quad whole and
+                // follows a grandchild slot from it before the child's head is
+                // checked, so the words past the arity must hold slot 0 (a
+                // stale slot id would be dereferenced; store_args and the
+                // loader keep the same invariant)
 #pragma unroll
                 for (int q = 0; q < MAXA / 4; ++q)
-                    if ((uint32_t)(q * 4) < iar)
+                    if (q == 0 || (uint32_t)(q * 4) < iar)
                         *reinterpret_cast<uint4*>(F + kWArgs + q * 4) =
                             make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
             } else {
@@ -1138,6 +1143,16 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
     }
 }
 
+// Grid sweep s claims through counter s & 3, which grid sweep s - 2 zeroes
+// (every CTA has read it by then).  Single-CTA sweeps skip that ring, so on
+// hand-back CTA 0 zeroes the counters of the next two sweeps itself (before
+// the grid barrier that releases them); a stale count would move the bump
+// over slots nobody writes, and the collector would keep their old records.
+__device__ __forceinline__ void zero_next_claims(const Params& P, uint32_t sweep) {
+    P.blocksum[kMaxGrid + ((sweep + 1) & 3)] = 0;
+    P.blocksum[kMaxGrid + ((sweep + 2) & 3)] = 0;
+}
+
 // CTA 0 runs sweeps out of shared memory while the frontier is small.
 template <int W>
 __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bool& just_collected,
@@ -1147,7 +1162,10 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     const uint32_t exit_m = min(P.small_exit, cap_m);
     if (F.M > exit_m) {
         // too wide for the shared-memory lists; nothing touched
-        if (threadIdx.x == 0) store_local(L, ctl);
+        if (threadIdx.x == 0) {
+            zero_next_claims(P, L.sweep);
+            store_local(L, ctl);
+        }
         return;
     }
     const uint32_t* gin = P.list[L.cur];
@@ -1273,6 +1291,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         region_off(P, L.cur)[0] = 0;
         region_cnt(P, L.cur)[0] = m;
         ctl->nregions[L.cur] = 1;
+        zero_next_claims(P, L.sweep);
         store_local(L, ctl);
     }
 }

@@ -310,3 +310,101 @@ def many_rules(nrules: int = 40, depth: int = 8) -> str:
 
     lines.append(f"input {tree(depth, 1)};")
     return "\n".join(lines) + "\n"
+
+
+def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: int = 4, calls: int = 64) -> str:
+    """A test family (not a BASELINE config): a random terminating system.
+
+    Constructors K0() | K1(T) | K2(T, T) and functions F0..F{nfun-1} of
+    arity 1-3, each defined by first-match rules on nested constructor
+    patterns (depth <= 2, some on the second argument too) with an optional
+    catch-all.  A right-hand side may call a lower function freely and its own
+    function only on a variable bound strictly inside the first argument's
+    pattern, so every system terminates (recursive path order with F_i > F_j
+    for i > j > constructors).  Inputs are random constructor terms under
+    random calls, `calls` of them joined by a balanced K2 tree (independent
+    redexes side by side, so the frontier widens past one warp)."""
+    rng = SplitMix64(seed * 0x9E3779B1 + 17)
+
+    def rnd(n):
+        return rng.next() % n
+
+    arity = [1 + rnd(3) for _ in range(nfun)]
+    cons = [("K0", 0), ("K1", 1), ("K2", 2)]
+    lines = ["sort T = struct K0() | K1(T) | K2(T, T) | "
+             + " | ".join(f"F{i}({', '.join(['T'] * a)})" for i, a in enumerate(arity)) + ";"]
+    vars_ = [f"x{k}" for k in range(12)] + ["y1", "y2"]
+    lines.append("var " + " ".join(f"{v} : T;" for v in vars_))
+    lines.append("eqn")
+
+    def pattern(depth, fresh, inner):
+        # a constructor pattern; `inner` collects variables bound strictly inside it
+        c, a = cons[rnd(3)]
+        if a == 0:
+            return f"{c}()"
+        subs = []
+        for _ in range(a):
+            if depth > 1 and rnd(3) == 0:
+                subs.append(pattern(depth - 1, fresh, inner))
+            else:
+                v = fresh.pop(0)
+                inner.append(v)
+                subs.append(v)
+        return f"{c}({', '.join(subs)})"
+
+    def rhs(i, depth, scope, smaller):
+        choice = rnd(10)
+        if depth == 0 or choice < 3:
+            if scope and rnd(4) != 0:
+                return scope[rnd(len(scope))]
+            return "K0()"
+        if choice < 6:
+            c, a = cons[1 + rnd(2)]
+            return f"{c}({', '.join(rhs(i, depth - 1, scope, smaller) for _ in range(a))})"
+        if choice < 9 and smaller:
+            args = [smaller[rnd(len(smaller))]] + [rhs(i, depth - 1, scope, smaller) for _ in range(arity[i] - 1)]
+            return f"F{i}({', '.join(args)})"
+        if i > 0:
+            j = rnd(i)
+            return f"F{j}({', '.join(rhs(i, depth - 1, scope, smaller) for _ in range(arity[j]))})"
+        return "K0()"
+
+    for i in range(nfun):
+        seen = set()
+        for _ in range(1 + rnd(3)):
+            fresh = list(vars_[:12])
+            inner = []
+            first = pattern(2, fresh, inner)
+            rest = []
+            for _ in range(arity[i] - 1):
+                if rnd(4) == 0:
+                    rest.append(pattern(1, fresh, []))
+                else:
+                    rest.append(fresh.pop(0))
+            lhs = f"F{i}({', '.join([first] + rest)})"
+            if lhs in seen:
+                continue
+            seen.add(lhs)
+            scope = [v for v in vars_[:12] if v not in fresh]
+            lines.append(f"  {lhs} = {rhs(i, 3, scope, inner)};")
+        if rnd(6) != 0:
+            xs = vars_[: arity[i]]
+            lines.append(f"  F{i}({', '.join(xs)}) = {rhs(i, 2, xs, [])};")
+
+    def data(depth):
+        if depth == 0 or rnd(6) == 0:
+            return "K0()"
+        c, a = cons[1 + rnd(2)]
+        return f"{c}({', '.join(data(depth - 1) for _ in range(a))})"
+
+    def term(depth, top=False):
+        if depth == 0 or (not top and rnd(2) == 0):
+            return data(input_depth)
+        i = rnd(nfun)
+        return f"F{i}({', '.join(term(depth - 1) for _ in range(arity[i]))})"
+
+    items = [term(call_depth, True) for _ in range(calls)]
+    while len(items) > 1:
+        items = [f"K2({items[k]}, {items[k + 1]})" if k + 1 < len(items) else items[k] for k in range(0, len(items), 2)]
+    lines.append(f"input {items[0]};")
+    return "\n".join(lines) + "\n"

@@ -407,3 +407,24 @@ def test_slab_size_does_not_change_results(engine, name, slab):
     assert res.total_rewrites == g["rewrites"]
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
     np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+
+
+@pytest.mark.parametrize("mode", ["default", "grid_only", "no_warp", "gc1", "interp"])
+@pytest.mark.parametrize("seed", range(40))
+def test_random_programs_against_oracle(engine, seed, mode):
+    """Random terminating systems (workloads.random_program; the oracle
+    agrees with the reference on the same seeds, test_oracle.py) in every
+    execution mode: rewrites, sweeps, per-sweep widths and the normal form."""
+    from oracle import oracle as port
+
+    text = W.random_program(seed)
+    o = port.run_text(text)
+    opts = {"default": {}, "grid_only": {"disable_small": 1}, "no_warp": {"disable_warp_mode": 1},
+            "gc1": {"gc_interval": 1, "validate": 1}, "interp": {}}[mode]
+    opt = api.make_options(**opts)
+    if mode == "interp":
+        opt.reserved[1] = 2
+    res = api.normalize_texts(text, engine=engine, options=opt)
+    assert (res.total_rewrites, res.sweeps) == (o.rewrites, o.sweeps)
+    np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
+    np.testing.assert_array_equal(res.words[0], o.words[0])

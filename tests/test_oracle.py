@@ -96,3 +96,21 @@ def test_workload_counts_fixture_consistent():
     assert d["transform22"]["rewrites"] == 117_440_511 and d["transform22"]["sweeps"] == 96
     o = O.run_text(W.fib(18), words=False)
     assert d["fib18"]["A"] == o.accesses
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built here")
+@pytest.mark.parametrize("seed", range(40))
+def test_random_programs_match_reference(seed):
+    """Random terminating systems (workloads.random_program: nested and
+    multi-position patterns, first-match order, catch-alls, stuck calls):
+    the C restatement and the reference's own sweep engine agree on rewrites,
+    sweeps, per-sweep widths and the normal form."""
+    from paper_2009_07174_b200 import workloads as W
+
+    text = W.random_program(seed)
+    o = O.run_text(text)
+    r = ref.run(text, "sweep", workers=1)
+    assert o.status == 0 and r.status == 0
+    assert (o.rewrites, o.sweeps) == (r.rewrites, r.sweeps)
+    np.testing.assert_array_equal(o.widths, r.widths)
+    np.testing.assert_array_equal(o.words[0], r.words)
