@@ -312,12 +312,13 @@ def many_rules(nrules: int = 40, depth: int = 8) -> str:
     return "\n".join(lines) + "\n"
 
 
-def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: int = 4, calls: int = 64) -> str:
+def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: int = 4, calls: int = 64,
+                   max_arity: int = 3) -> str:
     """A test family (not a BASELINE config): a random terminating system.
 
     Constructors K0() | K1(T) | K2(T, T) and functions F0..F{nfun-1} of
     arity 1-3, each defined by first-match rules on nested constructor
-    patterns (depth <= 2, some on the second argument too) with an optional
+    patterns (depth <= 2, some on later arguments too) with an optional
     catch-all.  A right-hand side may call a lower function freely and its own
     function only on a variable bound strictly inside the first argument's
     pattern, so every system terminates (recursive path order with F_i > F_j
@@ -329,7 +330,7 @@ def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: i
     def rnd(n):
         return rng.next() % n
 
-    arity = [1 + rnd(3) for _ in range(nfun)]
+    arity = [1 + rnd(max_arity) for _ in range(nfun)]
     cons = [("K0", 0), ("K1", 1), ("K2", 2)]
     lines = ["sort T = struct K0() | K1(T) | K2(T, T) | "
              + " | ".join(f"F{i}({', '.join(['T'] * a)})" for i, a in enumerate(arity)) + ";"]

@@ -428,3 +428,23 @@ def test_random_programs_against_oracle(engine, seed, mode):
     assert (res.total_rewrites, res.sweeps) == (o.rewrites, o.sweeps)
     np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
     np.testing.assert_array_equal(res.words[0], o.words[0])
+
+
+@pytest.mark.parametrize("mode", ["default", "grid_only", "gc1", "interp"])
+@pytest.mark.parametrize("seed", range(30))
+def test_random_wide_programs_against_oracle(engine, seed, mode):
+    """Random systems with arities up to 7 (16-word records when any symbol
+    takes more than 4 arguments) against the oracle in several modes."""
+    from oracle import oracle as port
+
+    text = W.random_program(seed, max_arity=7, nfun=5, call_depth=2, calls=32, input_depth=5)
+    o = port.run_text(text)
+    opts = {"default": {}, "grid_only": {"disable_small": 1}, "gc1": {"gc_interval": 1, "validate": 1},
+            "interp": {}}[mode]
+    opt = api.make_options(**opts)
+    if mode == "interp":
+        opt.reserved[1] = 2
+    res = api.normalize_texts(text, engine=engine, options=opt)
+    assert (res.total_rewrites, res.sweeps) == (o.rewrites, o.sweeps)
+    np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
+    np.testing.assert_array_equal(res.words[0], o.words[0])

@@ -114,3 +114,17 @@ def test_random_programs_match_reference(seed):
     assert (o.rewrites, o.sweeps) == (r.rewrites, r.sweeps)
     np.testing.assert_array_equal(o.widths, r.widths)
     np.testing.assert_array_equal(o.words[0], r.words)
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built here")
+@pytest.mark.parametrize("seed", range(30))
+def test_random_wide_programs_match_reference(seed):
+    """Random systems with functions of arity up to 7 (16-word records on the
+    GPU): the C restatement and the reference's sweep engine agree."""
+    text = W.random_program(seed, max_arity=7, nfun=5, call_depth=2, calls=32, input_depth=5)
+    o = O.run_text(text)
+    r = ref.run(text, "sweep", workers=1)
+    assert o.status == 0 and r.status == 0
+    assert (o.rewrites, o.sweeps) == (r.rewrites, r.sweeps)
+    np.testing.assert_array_equal(o.widths, r.widths)
+    np.testing.assert_array_equal(o.words[0], r.words)
