@@ -313,7 +313,7 @@ def many_rules(nrules: int = 40, depth: int = 8) -> str:
 
 
 def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: int = 4, calls: int = 64,
-                   max_arity: int = 3) -> str:
+                   max_arity: int = 3, input_seed: int | None = None) -> str:
     """A test family (not a BASELINE config): a random terminating system.
 
     Constructors K0() | K1(T) | K2(T, T) and functions F0..F{nfun-1} of
@@ -324,7 +324,9 @@ def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: i
     pattern, so every system terminates (recursive path order with F_i > F_j
     for i > j > constructors).  Inputs are random constructor terms under
     random calls, `calls` of them joined by a balanced K2 tree (independent
-    redexes side by side, so the frontier widens past one warp)."""
+    redexes side by side, so the frontier widens past one warp).  With
+    `input_seed` the system is the one of `seed` and only the input differs
+    (several such texts batch as roots of one store)."""
     rng = SplitMix64(seed * 0x9E3779B1 + 17)
 
     def rnd(n):
@@ -404,6 +406,8 @@ def random_program(seed: int, nfun: int = 4, input_depth: int = 7, call_depth: i
         i = rnd(nfun)
         return f"F{i}({', '.join(term(depth - 1) for _ in range(arity[i]))})"
 
+    if input_seed is not None:
+        rng = SplitMix64(input_seed * 0x85EBCA77 + 3)  # same system, another input
     items = [term(call_depth, True) for _ in range(calls)]
     while len(items) > 1:
         items = [f"K2({items[k]}, {items[k + 1]})" if k + 1 < len(items) else items[k] for k in range(0, len(items), 2)]

@@ -448,3 +448,31 @@ def test_random_wide_programs_against_oracle(engine, seed, mode):
     assert (res.total_rewrites, res.sweeps) == (o.rewrites, o.sweeps)
     np.testing.assert_array_equal(res.widths, np.asarray(o.widths, np.uint64))
     np.testing.assert_array_equal(res.words[0], o.words[0])
+
+
+@pytest.mark.parametrize("mode", ["default", "grid_only", "grow", "fixed_gc"])
+@pytest.mark.parametrize("seed", range(20))
+def test_random_program_batches_against_oracle(engine, seed, mode):
+    """One random system, four inputs as the roots of one store: batch widths
+    and every root's normal form against the oracle; also from a store that
+    starts nearly full (growth), and with a fixed capacity that only fits by
+    collecting (or fails with Capacity exactly when the oracle's does)."""
+    from oracle import oracle as port
+
+    texts = [W.random_program(seed, input_seed=k) for k in range(1, 5)]
+    o = port.run_text(texts)
+    s = api.System(texts[0])
+    st = api.Store.load([api.System(t) for t in texts])
+    n = st.view()["n"]
+    engine.set_program(s)
+    opts = {"grid_only": {"disable_small": 1}, "fixed_gc": {"fixed_capacity": 1, "gc_interval": 2}}.get(mode, {})
+    cap = {"grow": n + 8, "fixed_gc": 2 * n + 4096}.get(mode, 0)
+    engine.load(st, capacity=cap)
+    stats = engine.run(api.make_options(validate=1, **opts))
+    assert (stats["total_rewrites"], stats["sweeps"]) == (o.rewrites, o.sweeps)
+    widths = engine.trace()["rewrites"]
+    np.testing.assert_array_equal(widths, np.asarray(o.widths, np.uint64))
+    for k in range(len(texts)):
+        np.testing.assert_array_equal(engine.canonical(k), o.words[k])
+    if mode == "grow":
+        assert stats["regrows"] >= 1
