@@ -92,6 +92,9 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
     grid_sync(P.ctl, nblocks, epoch);
     for (;;) {
         const uint32_t i = atomicAdd(head, 1u);
+        // at most bump - 1 items are ever pushed: a later index stays empty
+        // (and lies past the queue, which a small store's grid outnumbers)
+        if (i >= bump) break;
         uint32_t x = 0;
         uint32_t ns = 32;
         while ((x = ld_acquire(Q + i)) == 0u) {

@@ -476,3 +476,37 @@ def test_random_program_batches_against_oracle(engine, seed, mode):
         np.testing.assert_array_equal(engine.canonical(k), o.words[k])
     if mode == "grow":
         assert stats["regrows"] >= 1
+
+
+@pytest.mark.parametrize("gc_interval", [0, 2])
+@pytest.mark.parametrize("seed", range(20))
+def test_random_program_export(engine, seed, gc_interval):
+    """Device export of random batches: the live store only, the reference's
+    refcount invariant over it, zeros past every arity, all nf, and the
+    engine's normal forms (= the oracle's) unchanged by the export."""
+    from oracle import oracle as port
+
+    texts = [W.random_program(seed, input_seed=k) for k in range(1, 4)]
+    o = port.run_text(texts)
+    s = api.System(texts[0])
+    st = api.Store.load([api.System(t) for t in texts])
+    v = st.view()
+    engine.set_program(s)
+    engine.load(st)
+    engine.run(api.make_options(gc_interval=gc_interval))
+    out = engine.fetch_store(v["maxarity"], v["num_roots"])
+    n = out["n"]
+    ar_of = np.asarray([s.symbol_arity(f) for f in range(s.num_symbols)], np.int64)
+    ar = ar_of[out["hss"][:n].astype(np.int64)]
+    ar[0] = 0
+    counted = np.bincount(np.asarray(out["roots"], np.int64), minlength=n)
+    for j in range(v["maxarity"]):
+        col = out["args"][j, :n].astype(np.int64)
+        used = ar > j
+        assert ((col > 0) & (col < n))[used].all()
+        assert (col[~used] == 0).all()
+        counted += np.bincount(col[used], minlength=n)
+    np.testing.assert_array_equal(out["refcounts"][1:n], counted[1:])
+    assert (counted[1:] > 0).all() and out["nf"][1:n].all()
+    for k in range(len(texts)):
+        np.testing.assert_array_equal(engine.canonical(k), o.words[k])
