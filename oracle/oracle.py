@@ -76,7 +76,7 @@ def lib():
             raise FileNotFoundError(f"{LIB_PATH} not built (make -C oracle oracle)")
         L = ctypes.CDLL(LIB_PATH)
         P, U32, U64, I = ctypes.c_void_p, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_int
-        for name in ("oracle_sweep", "oracle_seq"):
+        for name in ("oracle_sweep", "oracle_seq", "oracle_logical"):
             fn = getattr(L, name)
             fn.argtypes = [P, U32, P, U32, P, P, U32, P, U64, I, ctypes.POINTER(_Result)]
             fn.restype = I
@@ -101,9 +101,10 @@ def _run(fn_name: str, texts, step_budget: int = 0, words: bool = True) -> Oracl
                     counts={k: getattr(r.counts, k) for k, _ in Counts._fields_})
     if r.sweeps:
         out.widths = np.ctypeslib.as_array(r.widths, (r.sweeps,)).copy()
-        out.live = np.ctypeslib.as_array(r.live, (r.sweeps,)).copy()
-        out.n = np.ctypeslib.as_array(r.n, (r.sweeps,)).copy()
-        out.free_len = np.ctypeslib.as_array(r.free_len, (r.sweeps,)).copy()
+        if r.live:  # oracle_sweep only
+            out.live = np.ctypeslib.as_array(r.live, (r.sweeps,)).copy()
+            out.n = np.ctypeslib.as_array(r.n, (r.sweeps,)).copy()
+            out.free_len = np.ctypeslib.as_array(r.free_len, (r.sweeps,)).copy()
     if r.words:
         for k in range(r.num_roots):
             out.words.append(np.ctypeslib.as_array(r.words[k], (r.n_words[k],)).copy())
@@ -115,6 +116,12 @@ def _run(fn_name: str, texts, step_budget: int = 0, words: bool = True) -> Oracl
 def run_text(texts, step_budget: int = 0, words: bool = True) -> OracleRun:
     """Reference sweep engine (workers = 1) restated in C."""
     return _run("oracle_sweep", texts, step_budget, words)
+
+
+def run_logical(texts, step_budget: int = 0, words: bool = True) -> OracleRun:
+    """Reference sweep engine restated in logical time (dependency order, no
+    sweep-by-sweep scans): same widths, sweeps, rewrites and words."""
+    return _run("oracle_logical", texts, step_budget, words)
 
 
 def run_seq(texts, step_budget: int = 0, words: bool = True) -> OracleRun:

@@ -534,6 +534,163 @@ int oracle_seq(const trs_gpu_program* prog, uint32_t n, const uint32_t* roots, u
     return status;
 }
 
+/* ---- logical-time sweep engine ------------------------------------------
+ *
+ * The reference sweep engine (sweep_engine.cpp:69-258) re-examines every
+ * slot every sweep.  Slot i rewrites (or is marked nf) in sweep t exactly
+ * when, at the start of t,
+ *   (a) it is live and not nf (:164-171; garbage is always nf, SURVEY.md
+ *       §3b.10, so "not nf" implies live),
+ *   (b) it was not claimed or rewritten in place during an earlier part of
+ *       t (fresh slots lie at >= region_n and recycled ones read rc_read == 0,
+ *       :86, :156; a rewritten root is visited once per sweep, :153-161), and
+ *   (c) every argument is nf_read, i.e. became nf in a sweep before t
+ *       (:80-81, :173-178).
+ * All three are functions of event times: with b(i) the sweep in which i was
+ * built or last rewritten in place (0 for the input) and e(c) the sweep in
+ * which argument c became nf, i derives at
+ *       T(i) = max(b(i) + 1, max_j e(arg_j) + 1),
+ * and what it does there depends only on its own content and its nf
+ * arguments (nf slots never change, :170, :202-215).  So the reference's
+ * per-sweep widths, sweep count, rewrite total and normal form follow from
+ * processing slots in ANY order that respects those dependencies: a slot
+ * with a non-nf argument subscribes to it and is re-examined when it turns
+ * nf.  This is the semantics the B200 engine's barrier-free run-ahead relies
+ * on; tests/test_oracle.py pins it against the reference sweep engine's
+ * traces (the golden fixtures) and oracle_sweep. */
+int oracle_logical(const trs_gpu_program* prog, uint32_t n, const uint32_t* roots, uint32_t num_roots,
+                   const uint32_t* hss, const uint32_t* args, uint32_t max_arity, const uint32_t* refcounts,
+                   uint64_t step_budget, int want_words, oracle_result* out) {
+    memset(out, 0, sizeof(*out));
+    if (!step_budget) step_budget = 1000000000ull;
+    Prog P;
+    prog_init(&P, prog);
+    const uint32_t* arity = prog->arity;
+    Graph g;
+    memset(&g, 0, sizeof(g));
+    g.maxarity = max_arity;
+    for (uint32_t i = 0; i < n; ++i) g_new(&g, hss[i]);
+    for (uint32_t i = 1; i < n; ++i)
+        for (uint32_t j = 0; j < arity[hss[i]]; ++j) g_kids(&g, i)[j] = args[(size_t)j * n + i];
+    /* per node: nf epoch (g.nf, 0 = not nf), earliest derive sweep, waiter list */
+    vec32 tmin = {0}, whead = {0}, wnext = {0};
+    for (uint32_t i = 0; i < n; ++i) {
+        push32(&tmin, 1);
+        push32(&whead, 0);
+        push32(&wnext, 0);
+    }
+    vec64 hist = {0};
+    vec32 work = {0};
+    for (uint32_t i = n; i-- > 1;)
+        if (refcounts[i]) push32(&work, i);
+    uint32_t bind[ORACLE_MAX_VARS];
+    uint32_t built[ORACLE_MAX_INSTRS];
+    uint64_t rewrites = 0;
+    uint32_t last = 0; /* latest sweep with an event */
+    int status = 0;
+    double t0 = now_s();
+#define WAKE(x)                                        \
+    do {                                               \
+        for (uint32_t w_ = whead.v[x]; w_;) {          \
+            uint32_t nx_ = wnext.v[w_];                \
+            push32(&work, w_);                         \
+            w_ = nx_;                                  \
+        }                                              \
+        whead.v[x] = 0;                                \
+    } while (0)
+    while (work.n && !status) {
+        uint32_t x = work.v[--work.n];
+        if (g.nf.v[x]) continue;
+        uint32_t f = g.sym.v[x], ar = arity[f];
+        uint32_t T = tmin.v[x], pending = 0;
+        for (uint32_t j = 0; j < ar; ++j) {
+            uint32_t c = g_kids(&g, x)[j];
+            if (!g.nf.v[c]) {
+                pending = c;
+                break;
+            }
+            if (g.nf.v[c] + 1 > T) T = g.nf.v[c] + 1;
+        }
+        if (pending) { /* sleep on the first non-nf argument (the reference's scan stops there, :173-178) */
+            wnext.v[x] = whead.v[pending];
+            whead.v[pending] = x;
+            continue;
+        }
+        if (T > last) last = T;
+        int rule = try_rules(&P, f, x, &g, g_head, g_child, bind, NULL);
+        if (rule < 0) { /* no match: nf from this sweep on (:182-186) */
+            g.nf.v[x] = T;
+            WAKE(x);
+            continue;
+        }
+        while (hist.n <= T) push64(&hist, 0);
+        hist.v[T]++;
+        if (++rewrites > step_budget) {
+            status = TRS_GPU_STEP_BUDGET;
+            break;
+        }
+        const trs_gpu_rule* R = &prog->rules[rule];
+        if (!(R->root_ref & TRS_GPU_REF_NODE)) { /* collapse: copy, nf (:202-215) */
+            uint32_t src = bind[R->root_ref];
+            g.sym.v[x] = g.sym.v[src];
+            memcpy(g_kids(&g, x), g_kids(&g, src), sizeof(uint32_t) * (max_arity ? max_arity : 1));
+            g.nf.v[x] = T;
+            WAKE(x);
+            continue;
+        }
+        /* constructive: fresh nodes and the root in place, all derivable from T + 1 (:217-249) */
+        uint32_t nnew = R->num_instrs - 1;
+        for (uint32_t k = 0; k <= nnew; ++k) {
+            const trs_gpu_instr* I = &prog->instrs[R->first_instr + k];
+            uint32_t at = x;
+            if (k < nnew) {
+                at = g_new(&g, I->symbol);
+                push32(&tmin, T + 1);
+                push32(&whead, 0);
+                push32(&wnext, 0);
+                built[k] = at;
+            }
+            uint32_t tmp[64];
+            uint32_t iar = arity[I->symbol];
+            for (uint32_t q = 0; q < iar; ++q) {
+                uint32_t ref = prog->refs[I->first_ref + q];
+                tmp[q] = (ref & TRS_GPU_REF_NODE) ? built[ref & 0x7fffffffu] : bind[ref];
+            }
+            g.sym.v[at] = I->symbol;
+            for (uint32_t q = 0; q < iar; ++q) g_kids(&g, at)[q] = tmp[q];
+            push32(&work, at);
+        }
+        tmin.v[x] = T + 1;
+    }
+#undef WAKE
+    out->seconds = now_s() - t0;
+    out->status = status;
+    out->rewrites = rewrites;
+    out->num_roots = num_roots;
+    /* the run ends at the first sweep after the last event (:147) */
+    out->sweeps = status ? 0 : last + 1;
+    if (!status) {
+        out->widths = calloc(out->sweeps, sizeof(uint64_t));
+        for (uint32_t t = 1; t < hist.n && t <= last; ++t) out->widths[t - 1] = hist.v[t];
+    }
+    if (want_words && status == 0) {
+        out->words = calloc(num_roots, sizeof(uint32_t*));
+        out->n_words = calloc(num_roots, sizeof(uint64_t));
+        for (uint32_t r = 0; r < num_roots; ++r)
+            canonical(roots[r], (uint32_t)g.sym.n, arity, &g, g_head, g_child, &out->words[r], &out->n_words[r]);
+    }
+    free(g.sym.v);
+    free(g.kids.v);
+    free(g.nf.v);
+    free(tmin.v);
+    free(whead.v);
+    free(wnext.v);
+    free(hist.v);
+    free(work.v);
+    free(P.step_depth);
+    return status;
+}
+
 void oracle_free(oracle_result* r) {
     free(r->widths);
     free(r->live);

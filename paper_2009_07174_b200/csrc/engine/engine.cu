@@ -312,6 +312,14 @@ int fail(trs_gpu_engine* e, int code, const std::string& msg) {
     return code;
 }
 
+// Entry points that read or replace device state refuse while a run is
+// pending (trs_gpu_run_async .. trs_gpu_run_wait): the step loop may be
+// relaunched on the same buffers between the two.
+#define REFUSE_PENDING(e)                                                            \
+    do {                                                                              \
+        if ((e)->run.active) return fail((e), TRS_GPU_INVALID, "a run is pending (call trs_gpu_run_wait first)"); \
+    } while (0)
+
 #define CUDA_TRY(e, call)                                                              \
     do {                                                                              \
         cudaError_t err_ = (call);                                                    \
@@ -1013,6 +1021,36 @@ int fetch_arena(trs_gpu_engine* e, HostArena& h, std::vector<uint32_t>& roots) {
     return TRS_GPU_OK;
 }
 
+// Post-run refcount ghost invariant (sweep_engine.cpp:335-359): rc of every
+// uncollected slot = references from uncollected slots + root pins, and no
+// live slot references slot 0 or a collected slot.
+int validate_store(trs_gpu_engine* e) {
+    HostArena h;
+    std::vector<uint32_t> roots;
+    if (int r = fetch_arena(e, h, roots)) return r;
+    std::vector<uint64_t> counted(h.base, 0);
+    for (uint32_t i = 1; i < h.base; ++i) {
+        const uint32_t* R = h.rec(i);
+        if (R[kWHead] == kDeadHead) continue;
+        uint32_t ar = e->arity[R[kWHead] & kSymMask];
+        for (uint32_t j = 0; j < ar; ++j) {
+            uint32_t ch = R[kWArgs + j];
+            if (ch == 0 || ch >= h.base || h.rec(ch)[kWHead] == kDeadHead)
+                return fail(e, TRS_GPU_DANGLING, "slot " + std::to_string(i) + " references invalid slot " + std::to_string(ch));
+            counted[ch]++;
+        }
+    }
+    for (uint32_t r2 : roots) counted[r2]++;
+    for (uint32_t i = 1; i < h.base; ++i) {
+        const uint32_t* R = h.rec(i);
+        if (R[kWHead] == kDeadHead) continue;
+        if (counted[i] != R[kWRc])
+            return fail(e, TRS_GPU_DANGLING, "refcount ghost invariant: slot " + std::to_string(i) + " has rc " +
+                                                 std::to_string(R[kWRc]) + ", expected " + std::to_string(counted[i]));
+    }
+    return TRS_GPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1085,6 +1123,7 @@ void trs_gpu_close(trs_gpu_engine* e) {
 
 int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!e) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     int rc = build_blob(e, p);
     if (rc) return rc;
@@ -1138,6 +1177,7 @@ int trs_gpu_jit_info(trs_gpu_engine* e, int* active, double* seconds, char* log,
 int trs_gpu_load(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num_roots, const uint32_t* hss,
                  const uint32_t* args, uint32_t max_arity, const uint32_t* refcounts, uint64_t capacity) {
     if (!e || !hss || !refcounts || (max_arity && !args) || !roots) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     // H2D into a grow-only staging buffer owned by the engine (no per-call
     // allocation: allocator round trips show up as e2e jitter)
@@ -1166,6 +1206,7 @@ int trs_gpu_load_device(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, ui
                         const uint32_t* d_hss, const uint32_t* d_args, uint32_t max_arity,
                         const uint32_t* d_refcounts, uint64_t capacity) {
     if (!e || !d_hss || !d_refcounts || !roots) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     return load_impl(e, n, roots, num_roots, d_hss, d_args, max_arity, d_refcounts, capacity);
 }
@@ -1307,34 +1348,7 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
         st.load_ms = e->load_ms;
     cudaGetLastError();
     e->last_sweeps = c.sweep - c.sweep0;
-    if (result == TRS_GPU_OK && opt.validate) {
-        // refcount ghost invariant (sweep_engine.cpp:335-359): rc of every
-        // uncollected slot = references from uncollected slots + root pins
-        HostArena h;
-        std::vector<uint32_t> roots;
-        int r = fetch_arena(e, h, roots);
-        if (r) return r;
-        std::vector<uint64_t> counted(h.base, 0);
-        for (uint32_t i = 1; i < h.base; ++i) {
-            const uint32_t* R = h.rec(i);
-            if (R[kWHead] == kDeadHead) continue;
-            uint32_t ar = e->arity[R[kWHead] & kSymMask];
-            for (uint32_t j = 0; j < ar; ++j) {
-                uint32_t ch = R[kWArgs + j];
-                if (ch == 0 || ch >= h.base || h.rec(ch)[kWHead] == kDeadHead)
-                    return fail(e, TRS_GPU_DANGLING, "slot " + std::to_string(i) + " references invalid slot " + std::to_string(ch));
-                counted[ch]++;
-            }
-        }
-        for (uint32_t r2 : roots) counted[r2]++;
-        for (uint32_t i = 1; i < h.base; ++i) {
-            const uint32_t* R = h.rec(i);
-            if (R[kWHead] == kDeadHead) continue;
-            if (counted[i] != R[kWRc])
-                return fail(e, TRS_GPU_DANGLING, "refcount ghost invariant: slot " + std::to_string(i) + " has rc " +
-                                                     std::to_string(R[kWRc]) + ", expected " + std::to_string(counted[i]));
-        }
-    }
+    if (result == TRS_GPU_OK && opt.validate) result = validate_store(e);
     if (stats) *stats = st;
     return result;
 }
@@ -1384,6 +1398,7 @@ void* trs_gpu_stream(trs_gpu_engine* e) { return e ? (void*)e->stream : nullptr;
 
 int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out26) {
     if (!e || !e->d_ctl || !out26) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     uint64_t* out12 = out26;
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
@@ -1397,11 +1412,14 @@ int trs_gpu_profile_counters(trs_gpu_engine* e, uint64_t* out26) {
 
 int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats) {
     if (!e || !e->loaded) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     Ctl c0;
     CUDA_TRY(e, cudaMemcpy(&c0, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     const int blocks = grid_blocks(e, 0);
+    // the compaction scatters into the twin arena, where an export stages its columns
+    e->exported = false;
     Params P = make_params(e, blocks);
     P.allow_gc = 1;
     P.compact_only = max_rounds ? max_rounds : 8;
@@ -1438,6 +1456,7 @@ int trs_gpu_compact(trs_gpu_engine* e, uint32_t max_rounds, trs_gpu_stats* stats
 
 int trs_gpu_overhead_probe(trs_gpu_engine* e, uint32_t iters, uint32_t mode, uint32_t max_blocks, double* ns_per_iter) {
     if (!e || !e->loaded || !ns_per_iter) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     int blocks = grid_blocks(e, 0);
@@ -1459,6 +1478,7 @@ int trs_gpu_overhead_probe(trs_gpu_engine* e, uint32_t iters, uint32_t mode, uin
 int trs_gpu_fetch_records(trs_gpu_engine* e, void* dst, uint64_t cap_bytes, uint64_t* bytes, uint32_t* record_words,
                           uint32_t* roots_out) {
     if (!e || !e->loaded) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     Ctl c;
     CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
@@ -1476,6 +1496,7 @@ int trs_gpu_fetch_records(trs_gpu_engine* e, void* dst, uint64_t cap_bytes, uint
 
 int trs_gpu_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count) {
     if (!e || !e->d_trace) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
     uint64_t n = std::min<uint64_t>(e->last_sweeps, e->trace_cap);
@@ -1487,6 +1508,7 @@ int trs_gpu_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, ui
 int trs_gpu_canonical(trs_gpu_engine* e, uint32_t root_index, uint32_t* words, uint64_t cap, uint64_t* n_words,
                       uint32_t* n_nodes) {
     if (!e || !e->loaded) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     if (root_index >= e->num_roots) return fail(e, TRS_GPU_INVALID, "root index out of range");
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
@@ -1602,6 +1624,7 @@ extern "C" {
 int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uint32_t* hss, uint32_t* args,
                         uint32_t* refcounts, uint8_t* nf, uint32_t cap) {
     if (!e || !e->loaded || !n) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (e->roots_out_cap < e->num_roots) {
         cudaFree(e->d_roots_out);

@@ -443,29 +443,24 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     if (total) {
         if (slab.end - slab.cur < total) {
             abandon_slab<W, kSolo>(arena, slab);
-            uint32_t size = max(C.slab, total);
+            const uint32_t size = max(C.slab, total);
             uint32_t off = 0;
-            if (lane == 0) {
-                off = atomicAdd(C.claim_ctr, size);
-                if ((uint64_t)C.bump + off + size > C.cap && P.fixed_capacity) {
-                    // a full slab does not fit: take exactly what this step needs
-                    size = total;
-                    off = atomicAdd(C.claim_ctr, size);
-                }
-            }
+            if (lane == 0) off = atomicAdd(C.claim_ctr, size);
             off = w_bcast<kSolo>(off, 0);
-            size = w_bcast<kSolo>(size, 0);
             const uint64_t start = (uint64_t)C.bump + off;
-            if (start + size > C.cap) {
-                // fixed capacity exhausted: the reference raises Capacity (sweep_engine.cpp:221-226)
+            if (start + total > C.cap) {
+                // not even this step's slots fit: the reference raises
+                // Capacity when get_new_index finds no slot (sweep_engine.cpp:221-226)
                 if (lane == 0) {
                     atomicExch(&P.ctl->abort_capacity, 1u);
                     if (C.abort_flag) *C.abort_flag = 1u;
                 }
                 if (act == kActBuild) act = kActNone;
             } else {
+                // a slab that runs past the capacity is cut at it (the sweep's
+                // fold clamps the bump pointer the same way, sweep_engine.cpp:94-98)
                 slab.cur = (uint32_t)start;
-                slab.end = (uint32_t)(start + size);
+                slab.end = (uint32_t)min(start + size, C.cap);
             }
         }
         if (slab.end - slab.cur >= total) {
@@ -1061,7 +1056,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                               cap, slab_size, bind_base(P, slist)};
                     const uint32_t width =
                         warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc1 * kSmallCap, prof, pc);
-                    L.bump += ss.claim;
+                    L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
                     L.peak_bump = max(L.peak_bump, L.bump);
                     L.total += width;
                     L.maxw = width > L.maxw ? width : L.maxw;
@@ -1119,7 +1114,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
         }
         __syncwarp();
-        L.bump += ss.claim;
+        L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
         L.peak_bump = max(L.peak_bump, L.bump);
         L.total += width;
         L.maxw = width > L.maxw ? width : L.maxw;
@@ -1256,7 +1251,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
                                                       profc, pc);
         const unsigned long long width = block_sum64(rw, sm);
-        L.bump += ss.claim;
+        L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
         L.peak_bump = max(L.peak_bump, L.bump);
         L.total += width;
         L.maxw = width > L.maxw ? width : L.maxw;
@@ -1472,7 +1467,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         unsigned long long width = 0;
         F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, &width);
         const uint32_t allocd = __ldcg(claim_ctr);
-        L.bump += allocd;
+        L.bump = (uint32_t)min((uint64_t)L.bump + allocd, P.capacity);  // n = min(n + next_fresh, capacity), sweep_engine.cpp:94-98
         L.peak_bump = max(L.peak_bump, L.bump);
         L.total += width;
         L.maxw = width > L.maxw ? width : L.maxw;

@@ -128,3 +128,44 @@ def test_random_wide_programs_match_reference(seed):
     assert (o.rewrites, o.sweeps) == (r.rewrites, r.sweeps)
     np.testing.assert_array_equal(o.widths, r.widths)
     np.testing.assert_array_equal(o.words[0], r.words)
+
+
+@pytest.mark.parametrize("name", sorted(CASES))
+def test_logical_restatement_matches_reference_golden(name):
+    """The logical-time restatement (derive time T = max(built + 1, max
+    argument nf epoch + 1), dependency order, no sweep scans) reproduces the
+    reference sweep engine's trace exactly."""
+    g = CASES[name]
+    o = O.run_logical(g["text"])
+    assert o.status == 0
+    assert (o.rewrites, o.sweeps) == (g["rewrites"], g["sweeps"])
+    np.testing.assert_array_equal(o.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(o.words[0], np.asarray(g["words"], np.uint32))
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built here")
+@pytest.mark.parametrize("seed", range(0, 70, 3))
+def test_logical_random_programs_match_reference(seed):
+    text = W.random_program(seed) if seed % 2 == 0 else W.random_program(
+        seed, max_arity=7, nfun=5, call_depth=2, calls=32, input_depth=5)
+    o = O.run_logical(text)
+    r = ref.run(text, "sweep", workers=1)
+    assert o.status == 0 and r.status == 0
+    assert (o.rewrites, o.sweeps) == (r.rewrites, r.sweeps)
+    np.testing.assert_array_equal(o.widths, r.widths)
+    np.testing.assert_array_equal(o.words[0], r.words)
+
+
+def test_logical_matches_sweep_restatement_on_batches():
+    """Multi-root stores: both restatements agree per root and on widths."""
+    texts = [W.fib_batch(3, roots=64), W.fib_batch(5, roots=64)]
+    a, b = O.run_logical(texts), O.run_text(texts)
+    assert (a.rewrites, a.sweeps) == (b.rewrites, b.sweeps)
+    np.testing.assert_array_equal(a.widths, b.widths)
+    for x, y in zip(a.words, b.words):
+        np.testing.assert_array_equal(x, y)
+
+
+def test_logical_step_budget():
+    text = "sort T = A() | F(T);\nvar X : T;\neqn F(X) = F(F(X));\ninput F(A());\n"
+    assert O.run_logical(text, step_budget=500).status == 1
