@@ -1,21 +1,28 @@
 #!/usr/bin/env python
-"""Benchmark: config 5 of BASELINE.json -- 8 shards x 4096 independent fib
-roots (5F; `--workload sort` for the tree-merge-sort variant 5S), normalised
-on the B200 engine, shards split across the ranks (strong scaling).
+"""Benchmark: config 5 of BASELINE.json -- batches of 4096 independent fib
+roots per shard (5F; `--workload sort` for the tree-merge-sort variant 5S),
+normalised on the B200 engine, one process per GPU.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--scaling weak|strong] [--workload fib|sort]
 
-One step = one full normalisation of this rank's shards (all roots loaded as
-one multi-root store).  `value` = rewrites of all ranks / max-over-ranks
-device time, inputs already resident in HBM (device SoA -> engine load
-kernel -> step loop), L2 flushed before every step.  `e2e` = the same
-through the host C ABI with pinned host buffers: H2D of the SoA store, load,
-step loop, device compaction, D2H of the normal-form arena.
-"Measurement" for the roofline byte model.
+Scaling.  The path partitions into independent roots, so ranks share no
+data: by default every rank normalises 8 shards x 4096 roots of its own
+(rank r: seeds 8r+1..8r+8; "weak": the per-GPU work is config 5's 8 x 4096
+at every N).  `--scaling strong` splits one 8-shard batch over the ranks.
+
+One step = one full normalisation of this rank's shards, loaded as one
+multi-root store.  `value` = rewrites of all ranks / max-over-ranks device
+time, inputs already resident in HBM (device SoA -> load kernel -> step
+loop), L2 flushed before every step.  `e2e` = the same through the host C
+ABI with pinned host buffers: H2D of the SoA store, load, step loop, device
+export of the normal forms (mark, recount, renumber, pack) and their D2H in
+the reference TermStore layout.  DESIGN.md "Measurement" has the byte model.
 """
 import argparse
 import json
 import os
+import platform
 import statistics
 import subprocess
 import sys
@@ -29,7 +36,9 @@ import numpy as np  # noqa: E402
 
 METRIC = "rewrites/sec and achieved random-gather HBM GB/s (% of roofline) vs host CPU"
 COUNTS = os.path.join(ROOT, "tests", "golden", "workload_counts.json")
+FULLSIZE = os.path.join(ROOT, "tests", "golden", "fullsize_ref.json")
 PROFILE_SUMMARY = os.path.join(ROOT, "profiles", "traffic.json")
+SHARDS_PER_RANK = 8
 
 
 def parse_args():
@@ -39,9 +48,13 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--workload", choices=["fib", "sort"], default="fib")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak")
+    ap.add_argument("--dist-backend", choices=["nccl", "gloo"], default="nccl",
+                    help="backend of the two scalar reductions (gloo lets several ranks share one GPU)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the per-config single-GPU table")
-    ap.add_argument("--configs-only", action="store_true")
+    ap.add_argument("--cpu-sweep", action="store_true",
+                    help="also time the reference sweep engine (nproc workers) on the slow configs")
     ap.add_argument("--no-gate", action="store_true",
                     help="enqueue steps without the stream gate (needed under ncu, which serialises launches)")
     return ap.parse_args()
@@ -54,17 +67,30 @@ def dist_env():
     return world, rank, local
 
 
-def my_shards(rank: int, world: int, total: int = 8):
-    lo = rank * total // world
-    hi = (rank + 1) * total // world
-    return list(range(lo + 1, hi + 1))  # seeds
+def my_seeds(rank: int, world: int, scaling: str):
+    if scaling == "weak":
+        return list(range(SHARDS_PER_RANK * rank + 1, SHARDS_PER_RANK * (rank + 1) + 1))
+    lo = rank * SHARDS_PER_RANK // world
+    hi = (rank + 1) * SHARDS_PER_RANK // world
+    return list(range(lo + 1, hi + 1))
 
 
-def load_counts():
-    if os.path.exists(COUNTS):
-        with open(COUNTS) as f:
+def load_json(path):
+    if os.path.exists(path):
+        with open(path) as f:
             return json.load(f)
     return {}
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return platform.processor() or "unknown"
 
 
 class ClockSampler:
@@ -124,12 +150,17 @@ class ClockSampler:
 
 
 def measured_peaks():
-    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(p):
-        with open(p) as f:
-            d = json.load(f)
+    d = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"))
+    if d:
         return d.get("hbm_gbs", 6544.3), "measured"
     return 6650.0, "fallback"
+
+
+def workload_texts(kind: str, seeds):
+    from paper_2009_07174_b200 import workloads as W
+
+    mk = W.fib_batch if kind == "fib" else W.treemergesort_batch
+    return [mk(s) for s in seeds]
 
 
 def cpu_baseline_reference(texts):
@@ -143,7 +174,7 @@ def cpu_baseline_reference(texts):
         return {"value": sum(rewrites) / wall, "unit": "rewrites/s", "cores": len(texts), "kind": "reference",
                 "sample": f"{len(texts)} shards x 4096 roots, reference seq engine (seq_engine.cpp), "
                           f"one thread per shard, {wall:.2f} s wall", "seconds": wall,
-                "host_cpus": os.cpu_count()}
+                "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
     from oracle import oracle as port
 
     t = time.time()
@@ -153,10 +184,29 @@ def cpu_baseline_reference(texts):
     wall = time.time() - t
     return {"value": total / wall, "unit": "rewrites/s", "cores": 1, "kind": "port",
             "sample": "2 shards through the C oracle seq restatement, 1 thread", "seconds": wall,
-            "host_cpus": os.cpu_count()}
+            "host_cpus": os.cpu_count(), "cpu_model": cpu_model()}
 
 
-def run_reference(args, texts_all):
+def workload_config(args, shards_per_rank, world):
+    name = "fibbatch" if args.workload == "fib" else "treemergesort-batch"
+    tag = "5F" if args.workload == "fib" else "5S"
+    if args.scaling == "weak":
+        desc = (f"config {tag}: {name}, {shards_per_rank} shards x 4096 independent roots per GPU "
+                f"(rank r: seeds 8r+1..8r+8), {world} GPU(s)")
+    else:
+        desc = f"config {tag}: {name} 8 shards x 4096 independent roots (seeds 1..8) split over {world} GPU(s)"
+    return {"workload": desc, "shards_per_gpu": shards_per_rank, "roots_per_shard": 4096,
+            "parallelism": "shards (no inter-GPU traffic)",
+            "l2": "flushed between timed steps (512 MiB write on the engine stream)"}
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU rewriter (oracle/_ref, the
+    unmodified reference compiled from its sources) on this host's cores,
+    same metric.  Each step normalises a bounded sample of the workload: as
+    many shards as there are host threads (at most all shards of all ranks),
+    one thread per shard, concurrently; value = rewrites / wall of the engine
+    calls (bench.cpp:56-61)."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -165,88 +215,107 @@ def run_reference(args, texts_all):
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtrs_ref.so not built"}))
         return
+    total_shards = SHARDS_PER_RANK * world if args.scaling == "weak" else SHARDS_PER_RANK
+    k = max(1, min(total_shards, os.cpu_count() or 1))
+    texts = workload_texts(args.workload, list(range(1, k + 1)))
     vals = []
-    total_rw = 0
-    for k in range(args.warmup + args.steps):
-        wall, rw, st = ref.run_many(texts_all, "seq")
+    for step in range(args.warmup + args.steps):
+        wall, rw, st = ref.run_many(texts, "seq")
         assert all(s == 0 for s in st)
-        if k >= args.warmup:
+        if step >= args.warmup:
             vals.append((sum(rw), wall))
-            total_rw = sum(rw)
     t = sum(w for _, w in vals)
     value = sum(r for r, _ in vals) / t
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "rewrites/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / len(vals),
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": workload_config(args, len(texts_all)),
-        "cpu_baseline": {"value": value, "unit": "rewrites/s", "cores": len(texts_all), "kind": "reference",
-                         "sample": f"{len(texts_all)} shards, unmodified reference seq engine, one thread per "
-                                   f"shard, full workload per step ({total_rw} rewrites)",
-                         "host_cpus": os.cpu_count()},
+        "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic", "config": workload_config(args, SHARDS_PER_RANK, world),
+        "cpu_baseline": {"value": value, "unit": "rewrites/s", "cores": k, "kind": "reference",
+                         "sample": f"{k} shards (seeds 1..{k}) of the workload per step, unmodified reference seq "
+                                   f"engine, one thread per shard, concurrently",
+                         "host_cpus": os.cpu_count(), "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "rewrites/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
 
 
-def workload_config(args, nshards):
-    name = "fibbatch" if args.workload == "fib" else "treemergesort-batch"
-    return {"workload": f"config 5{'F' if args.workload == 'fib' else 'S'}: {name} {nshards} shards x 4096 "
-                        f"independent roots (seeds 1..{nshards})",
-            "shards": nshards, "roots_per_shard": 4096, "parallelism": "shards (no inter-GPU traffic)",
-            "l2": "flushed between timed steps (512 MiB write on the engine stream)"}
+def gather_curve(device, api):
+    """The random-gather roofline over footprint, access size and gathers in
+    flight per thread (trs_gpu_gather_probe_ex)."""
+    out = []
+    for fp in (256 << 20, 1 << 30, 4 << 30, 16 << 30):
+        for b in (4, 8, 32):
+            for ilp in (4, 16):
+                g = api.gather_probe(device, fp, b, 2, ilp=ilp)
+                out.append({"footprint_mib": fp >> 20, "bytes": b, "ilp": ilp, "gbps": round(g, 1),
+                            "g_accesses_per_s": round(g / b, 2)})
+    return out
 
 
-def per_config_table(eng, api, W, counts, hbm_peak, gather_gbps):
-    """Single-GPU timing + parity of every BASELINE config (one warm-up, one
-    timed run).  Rooflines: `gather_frac` is the SURVEY 8(d) model (4 B x A
-    against the measured uniformly random 4-B gather); it can exceed 1 where
-    part of the accesses hit L2 (build+sum: ~50 % L2 hit rate in ncu), so
-    `dram_frac` -- the ncu-measured DRAM bytes of the same launch
-    (profiles/traffic.json) over the run time, against the measured HBM copy
-    bandwidth -- is given beside it where a capture exists."""
+def per_config_table(eng, api, W, counts, fullsize, hbm_peak, gather_gbps, cpu_sweep):
+    """Single-GPU timing + bit-exact parity of every BASELINE config (one
+    warm-up, best of two timed runs), with the reference's CPU engines timed
+    on this host: seq (1 core, every config) and sweep (nproc workers; the
+    configs it finishes in seconds unless --cpu-sweep).  Rooflines:
+    `gather_frac` is the SURVEY 8(d) model (4 B x A against the measured
+    uniformly random 4-B gather); it can exceed 1 where accesses hit L2, so
+    `dram_frac` (ncu DRAM bytes of the same launch, profiles/traffic.json,
+    over the run time against the measured HBM copy bandwidth) and the
+    sector efficiency (4 A + S_min) / DRAM bytes sit beside it."""
     import hashlib
 
     import torch
 
-    traffic = {}
-    if os.path.exists(PROFILE_SUMMARY):
-        with open(PROFILE_SUMMARY) as f:
-            traffic = json.load(f)
+    from oracle import ref
+
+    traffic = load_json(PROFILE_SUMMARY)
     out = {}
+    nproc = os.cpu_count() or 1
     names = ["fib18", "mergesort16k", "transform22", "buildsum22", "reverse16k", "ackermann36", "sortbatch"]
+    # the reference sweep engine takes minutes on these at nproc workers (SURVEY §6)
+    slow_sweep = {"mergesort16k", "buildsum22", "sortbatch"}
     for name in names:
         if name == "sortbatch":
-            texts = [W.treemergesort_batch(s) for s in range(1, 9)]
-            systems = [api.System(t) for t in texts]
-            sysm = systems[0]
-            store = api.Store.load(systems)
+            texts = W.batch_shards("sort")
             keys = [f"sortbatch_s{s}" for s in range(1, 9)]
             tkey = "sortbatch_8shards"
         else:
-            sysm = api.System(W.CONFIGS[name][0]())
-            store = api.Store.load(sysm)
+            texts = [W.CONFIGS[name][0]()]
             keys = [name]
             tkey = name
-        eng.set_program(sysm)
+        t0 = time.perf_counter()
+        systems = [api.System(t) for t in texts]
+        t1 = time.perf_counter()
+        store = api.Store.load(systems)
+        t2 = time.perf_counter()
+        eng.set_program(systems[0])
         best = None
-        for rep in range(2):
+        for _ in range(3):
             eng.load(store)
             st = eng.run()
-            best = st
-        tr = eng.trace()
-        widths = tr["rewrites"].astype("<u8")
+            if best is None or st["kernel_ms"] < best["kernel_ms"]:
+                best = st
+        widths = eng.trace()["rewrites"].astype("<u8")
+        canon = eng.canonical_all(len(keys), words=False)
+        fx = [fullsize.get(k) for k in keys]
         cs = [counts.get(k) for k in keys]
         t = best["kernel_ms"] * 1e-3
         row = {"rewrites": best["total_rewrites"], "sweeps": best["sweeps"], "kernel_ms": best["kernel_ms"],
                "rewrites_per_s": best["total_rewrites"] / t, "us_per_sweep": 1e6 * t / best["sweeps"],
-               "small_sweeps": best["small_sweeps"], "gc_runs": best["gc_runs"]}
+               "small_sweeps": best["small_sweeps"], "gc_runs": best["gc_runs"],
+               "phys_sweeps": int(len(eng.phys_trace())),
+               "host_parse_ms": round(1e3 * (t1 - t0), 2), "host_flatten_ms": round(1e3 * (t2 - t1), 2)}
+        if all(fx):
+            row["parity"] = {
+                "rewrites": sum(f["rewrites"] for f in fx) == best["total_rewrites"],
+                "words": all(str(int(canon["hashes"][k])) == fx[k].get("words_hash") for k in range(len(keys))),
+                "sweeps": max(f.get("sweeps", 0) for f in fx) == best["sweeps"],
+            }
+            if len(keys) == 1 and "widths_sha1" in fx[0]:
+                row["parity"]["widths"] = fx[0]["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
+            row["parity"]["source"] = "tests/golden/fullsize_ref.json (unmodified reference, make_fullsize.py)"
         if all(cs):
-            row["parity_rewrites"] = sum(c["rewrites"] for c in cs) == best["total_rewrites"]
-            if len(cs) == 1:
-                row["parity_widths"] = cs[0]["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
-            else:
-                row["parity_sweeps"] = max(c["sweeps"] for c in cs) == best["sweeps"]
             a = sum(c["A"] for c in cs)
             smin = sum(c["S_min"] for c in cs)
             row["gather_gbps"] = 4 * a / t / 1e9
@@ -255,12 +324,57 @@ def per_config_table(eng, api, W, counts, hbm_peak, gather_gbps):
             row["dram_model_frac"] = row["dram_model_gbps"] / hbm_peak
             t_roof = max(4 * a / (gather_gbps * 1e9) if gather_gbps else 0, smin / (hbm_peak * 1e9))
             row["t_roof_frac"] = t_roof / t
+            if tkey in traffic:
+                row["sector_efficiency"] = (4 * a + smin) / traffic[tkey]
         if tkey in traffic:
             row["dram_gbps"] = traffic[tkey] / t / 1e9
             row["dram_frac"] = row["dram_gbps"] / hbm_peak
+        # the reference's CPU engines on this host (engine time only, bench.cpp:56-61)
+        if ref.available():
+            if len(texts) == 1:
+                sq = ref.run(texts[0], "seq", words=False)
+                row["cpu_seq_s"] = sq.micros * 1e-6
+                if name not in slow_sweep or cpu_sweep:
+                    sw = ref.run(texts[0], "sweep", workers=nproc, words=False)
+                    row["cpu_sweep_s"] = sw.micros * 1e-6
+                    row["cpu_sweep_workers"] = nproc
+            else:
+                wall, rw, _ = ref.run_many(texts, "seq")
+                row["cpu_seq_s"] = wall
+                row["cpu_seq_note"] = f"{len(texts)} shards, one thread each, concurrently"
+            if "cpu_seq_s" in row:
+                row["gpu_vs_cpu_seq"] = row["cpu_seq_s"] / t
         out[name] = row
-        del store, sysm
+        del store, systems
         torch.cuda.synchronize()
+    return out
+
+
+def gc_at_scale(eng, api, W, fullsize):
+    """Compacting GC on the large configs: a fixed capacity below the run's
+    allocation forces in-loop collections (term_store.cpp:140-157's role);
+    parity and the collection time are reported."""
+    out = {}
+    for name, texts, keys, cap in (("buildsum22", [W.buildsum(22)], ["buildsum22"], 36 << 20),
+                                   ("fibbatch", W.batch_shards("fib"), [f"fibbatch_s{s}" for s in range(1, 9)],
+                                    48 << 20)):
+        systems = [api.System(t) for t in texts]
+        store = api.Store.load(systems)
+        eng.set_program(systems[0])
+        eng.load(store, capacity=cap)
+        try:
+            st = eng.run(api.make_options(fixed_capacity=1))
+        except api.EngineError as e:
+            out[name] = {"capacity_slots": cap, "error": str(e)}
+            continue
+        canon = eng.canonical_all(len(keys), words=False)
+        fx = [fullsize.get(k) for k in keys]
+        out[name] = {"capacity_slots": cap, "kernel_ms": st["kernel_ms"], "gc_runs": st["gc_runs"],
+                     "gc_ms": st["gc_ms"], "peak_slots": st["peak_slots"],
+                     "rewrites_match": st["total_rewrites"] == sum(f["rewrites"] for f in fx),
+                     "words_match": all(str(int(canon["hashes"][k])) == fx[k].get("words_hash")
+                                        for k in range(len(keys)))}
+        del store, systems
     return out
 
 
@@ -269,31 +383,45 @@ def main():
     world, rank, local = dist_env()
     from paper_2009_07174_b200 import workloads as W
 
-    kind = args.workload
-    seeds_all = list(range(1, 9))
-    mk = W.fib_batch if kind == "fib" else W.treemergesort_batch
     if args.impl == "reference":
-        run_reference(args, [mk(s) for s in seeds_all])
+        run_reference(args)
         return
 
     import torch
 
     from paper_2009_07174_b200 import api
 
-    torch.cuda.set_device(local)
+    ndev = torch.cuda.device_count()
+    dev_index = local % max(1, ndev)  # several ranks may share a GPU (gloo)
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    seeds = my_shards(rank, world)
-    texts = [mk(s) for s in seeds]
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+    red_dev = dev if args.dist_backend == "nccl" else torch.device("cpu")
+
+    def reduce(x, op):
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            torch.distributed.all_reduce(t, op=op)
+        return t.item()
+
+    seeds = my_seeds(rank, world, args.scaling)
+    t_in0 = time.perf_counter()
+    texts = workload_texts(args.workload, seeds)
     systems = [api.System(t) for t in texts]
+    t_in1 = time.perf_counter()
     store = api.Store.load(systems)
+    t_in2 = time.perf_counter()
     v = store.view()
-    eng = api.Engine(local)
+    eng = api.Engine(dev_index)
     eng.set_program(systems[0])
-    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
-    dev = torch.device("cuda", local)
+    jit = eng.jit_info()
+    stream = torch.cuda.ExternalStream(eng.stream, device=dev)
 
     # device-resident inputs (value path) and pinned host inputs (e2e path)
     d_hss = torch.from_numpy(v["hss"].view(np.int32)).to(dev)
@@ -331,13 +459,13 @@ def main():
 
     # ---- warm-up (also sizes the arena once so no growth happens inside timing)
     for _ in range(args.warmup):
-        st = step_value()
+        step_value()
     torch.cuda.synchronize()
 
     # ---- timed: device-resident inputs
     evs = []
     stats = []
-    with ClockSampler(local) as clocks:
+    with ClockSampler(dev_index) as clocks:
         if world > 1:
             torch.distributed.barrier()
         torch.cuda.synchronize()
@@ -351,33 +479,27 @@ def main():
         if world > 1:
             torch.distributed.barrier()
     step_ms = [a.elapsed_time(b) for a, b in evs]
-    my_ms = sum(step_ms)
-    my_rewrites = sum(s["total_rewrites"] for s in stats)
-    tot = torch.tensor([my_ms], dtype=torch.float64, device=dev)
-    rw = torch.tensor([my_rewrites], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(tot, op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(rw, op=torch.distributed.ReduceOp.SUM)
-    max_ms = tot.item()
-    all_rw = rw.item()
+    max_ms = reduce(sum(step_ms), torch.distributed.ReduceOp.MAX if world > 1 else None)
+    all_rw = reduce(sum(s["total_rewrites"] for s in stats), torch.distributed.ReduceOp.SUM if world > 1 else None)
     value = all_rw / (max_ms * 1e-3)
-    # load_records + load_frontier + init_ctl, then prep_launch + step loop per launch
-    launches = sum(3 + 2 * s["launches"] for s in stats)
+    # load_records + load_frontier + init_ctl, then prep_launch + step loop + finish_run per launch
+    launches = sum(3 + 3 * s["launches"] for s in stats)
 
     # ---- e2e: pinned host buffers through the C ABI: H2D of the SoA store,
     # run, and the normal form written back in the reference TermStore layout
-    # (trs_gpu_fetch_store: device compaction + pack + D2H of hss, args,
-    # refcounts, nf and roots)
+    # (trs_gpu_fetch_store: device export + D2H of hss, args, refcounts, nf, roots)
+    import ctypes
+
     h2d = (p_hss.numel() + p_args.numel() + p_rc.numel() + p_roots.numel()) * 4
-    d2h_bytes = []
-    e2e_ms = []
-    e2e_host = []  # host ms of load, run, export, fetch per step (diagnostics)
+    d2h_bytes, e2e_ms, e2e_host = [], [], []
     out = None
     ma = int(v["maxarity"])
     L = api.lib()
-    import ctypes
-    e2e_clocks = ClockSampler(local)
+    launches_e2e = 0
+    e2e_clocks = ClockSampler(dev_index)
     e2e_clocks.__enter__()
+    if world > 1:
+        torch.distributed.barrier()
     for k in range(args.warmup + args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(k & 0xFF)
@@ -414,44 +536,45 @@ def main():
             e2e_host.append([round(1e3 * (b - a), 3) for a, b in ((th0, th1), (th1, th2), (th2, th3), (th3, th4))])
             e2e_ms.append(e0.elapsed_time(e1))
             d2h_bytes.append(N * (4 + 4 * ma + 4 + 1) + 4 * len(roots))
-            launches_e2e = 3 + 2 * s_run["launches"] + 2  # load (3), prep + step loop(s), compaction, pack
+            launches_e2e = 3 + 3 * s_run["launches"] + 1  # load (3), prep + loop + finish per launch, export
     e2e_clocks.__exit__(None, None, None)
-    e2e_tot = torch.tensor([sum(e2e_ms)], dtype=torch.float64, device=dev)
-    if world > 1:
-        torch.distributed.all_reduce(e2e_tot, op=torch.distributed.ReduceOp.MAX)
-    e2e_value = all_rw / (e2e_tot.item() * 1e-3)
+    e2e_max = reduce(sum(e2e_ms), torch.distributed.ReduceOp.MAX if world > 1 else None)
+    e2e_value = all_rw / (e2e_max * 1e-3)
 
-    # parity of this rank's shards against the reference-derived fixture
-    counts = load_counts()
-    key = "fibbatch" if kind == "fib" else "sortbatch"
-    fx = [counts.get(f"{key}_s{s}") for s in seeds]
+    # ---- parity of this rank's shards against the reference fixture: every
+    # shard's normal form (device relabelling + hash), rewrites, sweeps
+    fullsize = load_json(FULLSIZE)
+    key = "fibbatch" if args.workload == "fib" else "sortbatch"
+    fx = [fullsize.get(f"{key}_s{s}") for s in seeds]
+    canon = eng.canonical_all(len(seeds), words=False)
     parity = None
     if all(fx):
-        parity = {"rewrites_match": int(sum(c["rewrites"] for c in fx)) == int(stats[-1]["total_rewrites"]),
-                  "reference_rewrites": int(sum(c["rewrites"] for c in fx)),
-                  "sweeps_match": max(c["sweeps"] for c in fx) == int(stats[-1]["sweeps"])}
+        words_ok = [str(int(canon["hashes"][k])) == fx[k].get("words_hash") for k in range(len(seeds))]
+        parity = {"shards": seeds, "words_match": words_ok,
+                  "rewrites_match": int(sum(f["rewrites"] for f in fx)) == int(stats[-1]["total_rewrites"]),
+                  "reference_rewrites": int(sum(f["rewrites"] for f in fx))}
+        if all("sweeps" in f for f in fx):
+            parity["sweeps_match"] = max(f["sweeps"] for f in fx) == int(stats[-1]["sweeps"])
+    ok = 1.0 if (parity and all(parity["words_match"]) and parity["rewrites_match"]) else 0.0
+    all_ok = reduce(ok, torch.distributed.ReduceOp.MIN if world > 1 else None)
 
     if rank != 0:
         if world > 1:
             torch.distributed.destroy_process_group()
         return
 
+    counts = load_json(COUNTS)
     hbm_peak, peak_kind = measured_peaks()
-    gather_gbps = api.gather_probe(local, 4 << 30, 4, 5)
-    # the same probe at 8/16/32 bytes per access: the random-access rate is
-    # the limit (flat up to 16 B), not bytes
-    gather_wide = {f"{b}B_gbps": api.gather_probe(local, 4 << 30, b, 3) for b in (8, 16, 32)}
+    gather_gbps = api.gather_probe(dev_index, 4 << 30, 4, 5)
     kernel_ms = statistics.mean(s["kernel_ms"] for s in stats)
+    cs = [counts.get(f"{key}_s{s}") for s in seeds]
     roofline = None
-    if all(fx):
-        A = sum(c["A"] for c in fx)
-        smin = sum(c["S_min"] for c in fx)
+    if all(cs):
+        A = sum(c["A"] for c in cs)
+        smin = sum(c["S_min"] for c in cs)
         t = kernel_ms * 1e-3
         alg_bytes = 32 * A + smin
-        traffic = None
-        if os.path.exists(PROFILE_SUMMARY):
-            with open(PROFILE_SUMMARY) as f:
-                traffic = json.load(f).get(f"{key}_{len(seeds)}shards")
+        traffic = load_json(PROFILE_SUMMARY).get(f"{key}_{len(seeds)}shards")
         roofline = {
             "bound": "hbm", "achieved": alg_bytes / t / 1e9, "peak": hbm_peak, "unit": "GB/s",
             "frac": alg_bytes / t / 1e9 / hbm_peak, "traffic": traffic,
@@ -460,45 +583,51 @@ def main():
             "byte_model": "32 B x A (one DRAM sector per random access) + S_min (frontier streaming), "
                           "SURVEY.md 8(d); A, S_min from the C oracle (tests/golden/workload_counts.json)",
             "peak_kind": peak_kind,
+            "sector_efficiency": (4 * A + smin) / traffic if traffic else None,
             "gather": {"achieved_gbps": 4 * A / t / 1e9, "roofline_gbps": gather_gbps,
                        "frac": 4 * A / t / 1e9 / gather_gbps,
                        "definition": "4 B x A / step-loop time vs measured uniformly random 4-B gather over "
-                                     "4 GiB (trs_gpu_gather_probe)",
-                       "accesses_per_s": A / t, "roofline_accesses_per_s": gather_gbps * 1e9 / 4,
-                       "probe_wider": gather_wide},
+                                     "4 GiB (trs_gpu_gather_probe, 4 gathers in flight per thread)",
+                       "accesses_per_s": A / t, "roofline_accesses_per_s": gather_gbps * 1e9 / 4},
             "t_roof_frac": max(4 * A / (gather_gbps * 1e9), smin / (hbm_peak * 1e9)) / t,
         }
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline_reference([mk(s) for s in seeds_all])
-    configs = None
+        cpu = cpu_baseline_reference(workload_texts(args.workload, list(range(1, SHARDS_PER_RANK + 1))))
+    configs = gc_rows = curve = None
     if world == 1 and not args.no_configs:
-        configs = per_config_table(eng, api, W, counts, hbm_peak, gather_gbps)
+        curve = gather_curve(dev_index, api)
+        configs = per_config_table(eng, api, W, counts, fullsize, hbm_peak, gather_gbps, args.cpu_sweep)
+        gc_rows = gc_at_scale(eng, api, W, fullsize)
     line = {
         "metric": METRIC, "value": value, "unit": "rewrites/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": workload_config(args, 8),
+        "warmup": args.warmup, "ms_per_step": max_ms / args.steps, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": workload_config(args, len(seeds), world),
         "roofline": roofline,
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "rewrites/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(statistics.mean(d2h_bytes)),
                 "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_fetch_store (device export: "
                         "mark from the roots, recount references, renumber, pack; D2H of the reference TermStore "
-                        "columns into pinned host memory), CUDA events on the engine stream", "ms_per_step": statistics.mean(e2e_ms),
-                "gpu_launches_per_step": launches_e2e,
-                "step_ms": [round(x, 3) for x in e2e_ms],
-                "clocks": e2e_clocks.summary(),
-                "host_ms_load_run_export_fetch": e2e_host[-1] if e2e_host else None},
+                        "columns into pinned host memory), CUDA events on the engine stream",
+                "ms_per_step": statistics.mean(e2e_ms), "gpu_launches_per_step": launches_e2e,
+                "step_ms": [round(x, 3) for x in e2e_ms], "clocks": e2e_clocks.summary(),
+                "host_ms_load_run_export_fetch": e2e_host[-1] if e2e_host else None,
+                "input_side_host_ms": {"parse_resolve": round(1e3 * (t_in1 - t_in0), 1),
+                                       "flatten_to_soa": round(1e3 * (t_in2 - t_in1), 1)}},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
-        "parity": parity,
+        "parity": parity, "parity_all_ranks": bool(all_ok), "rewrites_all_ranks": int(all_rw),
         "engine": {"sweeps": stats[-1]["sweeps"], "small_sweeps": stats[-1]["small_sweeps"],
                    "gc_runs": stats[-1]["gc_runs"], "grid_blocks": stats[-1]["grid_blocks"],
                    "block_threads": stats[-1]["block_threads"], "record_words": stats[-1]["record_words"],
-                   "peak_slots": stats[-1]["peak_slots"], "kernel_ms": kernel_ms,
-                   "step_ms": step_ms},
+                   "peak_slots": stats[-1]["peak_slots"], "kernel_ms": kernel_ms, "step_ms": step_ms,
+                   "jit_active": jit["active"], "nvrtc_compile_s": round(jit["seconds"], 3),
+                   "dist_backend": args.dist_backend if world > 1 else None},
+        "gather_curve": curve,
         "per_config": configs,
+        "gc_at_scale": gc_rows,
     }
     print(json.dumps(line))
     if world > 1:

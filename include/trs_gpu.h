@@ -118,15 +118,23 @@ typedef struct trs_gpu_options {
     uint32_t profile;          /* 1: accumulate per-phase cycle counters (trs_gpu_profile_counters); >1: only grid sweeps of <= profile entries */
     uint32_t disable_warp_mode; /* 1: frontiers <= 32 slots still run on the whole CTA */
     uint32_t reserved[4];       /* [0] zero; [1] bit 0: no shared-memory resident arena in
-                                   the single-CTA mode, bit 1: interpreted (not specialised) step loop;
-                                   [2] slab override (0); [3] zero */
+                                   the single-CTA mode, bit 1: interpreted (not specialised) step loop,
+                                   bit 2: no run-ahead (also off with an explicit step_budget or a fixed
+                                   capacity, or TRS_B200_RUNAHEAD=0); [2] slab override (0); [3] zero */
 } trs_gpu_options;
 
 /* Per-sweep record (reference SweepRecord, sweep_engine.hpp:10-17).
- * `rewrites` is the sweep width and is bit-exact to the reference;
- * live_terms/n/free_len are allocator-dependent there and here: n is the
- * arena bump pointer, free_len is always 0 (bump allocation + compaction
- * leaves no free list), `active` is the size of the awake frontier list. */
+ * trs_gpu_trace returns one record per LOGICAL sweep -- the reference's
+ * sweeps -- with `rewrites` the sweep width, bit-exact to the reference; the
+ * engine may run ahead of the sweep it physically executes (a lane carries on
+ * with a slot its own step made ready, at that slot's logical sweep), so the
+ * other fields are 0 there.  trs_gpu_phys_trace returns one record per
+ * PHYSICAL sweep (a step-loop iteration): rewrites performed in it, n = the
+ * arena bump pointer, live_terms = bump - 1 (allocated slots not yet
+ * reclaimed by a compaction; the reference's refcount > 0 count is
+ * trs_gpu_live_count), free_len = 0 (bump allocation leaves no free list),
+ * active = frontier entries, mode 0 grid-wide, 1 single-CTA, 2 warp / solo,
+ * 3 single-CTA over the shared-memory resident arena, and the duration. */
 typedef struct trs_gpu_sweep_record {
     uint32_t sweep;
     uint32_t live_terms;
@@ -134,7 +142,7 @@ typedef struct trs_gpu_sweep_record {
     uint32_t n;
     uint32_t free_len;
     uint32_t active;
-    uint32_t mode; /* 0 grid-wide sweep, 1 single-CTA sweep */
+    uint32_t mode;
     uint64_t micros_x1000; /* sweep duration in ns (device globaltimer) */
 } trs_gpu_sweep_record;
 
@@ -150,7 +158,7 @@ typedef struct trs_gpu_stats {
     uint32_t block_threads;
     uint32_t record_words;
     uint64_t peak_slots;       /* highest bump pointer reached */
-    uint64_t live_terms;       /* slots with refcount > 0 at the end */
+    uint64_t live_terms;       /* allocated slots at the end (bump - 1); exact refcount > 0 count: trs_gpu_live_count */
     double kernel_ms;          /* device time of the step-loop launches (CUDA events) */
     double gc_ms;              /* device time spent inside compacting GC (globaltimer) */
     double load_ms;            /* device time of the load kernel */
@@ -218,9 +226,13 @@ int trs_gpu_jit_info(trs_gpu_engine* engine, int* active, double* seconds, char*
 int trs_gpu_hold(trs_gpu_engine* engine);
 int trs_gpu_release(trs_gpu_engine* engine);
 
-/* Per-sweep records of the last run; *count receives the number of records
- * (copies min(count, cap)). */
+/* Per-sweep records of the last run, one per logical sweep (the reference's
+ * trace); *count receives the number of records (copies min(count, cap)). */
 int trs_gpu_trace(trs_gpu_engine* engine, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count);
+
+/* Per-physical-sweep records of the last run (diagnostics: duration, mode,
+ * frontier size, rewrites executed in that step-loop iteration). */
+int trs_gpu_phys_trace(trs_gpu_engine* engine, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count);
 
 /* Canonical DAG words of root `root_index` (pre-order from
  * the root, children left to right, ids on first visit, words = symbol then
@@ -229,6 +241,33 @@ int trs_gpu_trace(trs_gpu_engine* engine, trs_gpu_sweep_record* out, uint64_t ca
  * references slot 0 or a dead slot (term_store.cpp:84-88). */
 int trs_gpu_canonical(trs_gpu_engine* engine, uint32_t root_index, uint32_t* words, uint64_t cap,
                       uint64_t* n_words, uint32_t* n_nodes);
+
+/* Canonical words of EVERY root, computed on the device (canon.cuh; SURVEY.md
+ * §8(f)2) from the export of the current store: words of root r are
+ * words[root_offsets[r] .. root_offsets[r+1]); hashes[r] is a 64-bit
+ * position-keyed hash of them (sum over k of SplitMix64((k << 32) ^ w_k ^
+ * 0x9e3779b97f4a7c15)) for comparisons without the copy; root_nodes[r] the
+ * node count.  Any output pointer may be NULL; words are copied only when
+ * cap >= *n_words.  Replaces extract + relabelling (term_store.cpp:77-116). */
+int trs_gpu_canonical_all(trs_gpu_engine* engine, uint32_t* words, uint64_t cap, uint64_t* n_words,
+                          uint64_t* root_offsets, uint64_t* hashes, uint32_t* root_nodes);
+
+/* The program as staged on the device (read back from device memory),
+ * rendered in the reference's dump-dispatch format (dispatch.cpp:98-134), so
+ * it can be compared byte for byte with the reference's own dump of the same
+ * system.  Names come from the caller's signature: symbol_names[symbol],
+ * var_names[variable]; device rule r (rules in trs_gpu_program order) maps
+ * variable slot k to variable rule_vars[rule_var_begin[r] + k]; rule_texts
+ * [source_order] is "lhs = rhs" as the reference prints it.  Two-call
+ * protocol on cap (*need includes the terminating NUL). */
+int trs_gpu_dump_program(trs_gpu_engine* engine, const char* const* symbol_names, const char* const* var_names,
+                         const uint32_t* rule_var_begin, const uint32_t* rule_vars, const char* const* rule_texts,
+                         char* out, uint64_t cap, uint64_t* need);
+
+/* Exact count of slots with refcount > 0 in the current store: the
+ * reference's live_terms (sweep_engine.cpp:122-123), which includes
+ * garbage not yet collected. */
+int trs_gpu_live_count(trs_gpu_engine* engine, uint64_t* live);
 
 /* Raw store copy-back (reference TermStore layout): after a compacting pass
  * the live slots are renumbered 1..n-1 in their arena order, roots updated.
@@ -274,6 +313,12 @@ int trs_gpu_fetch_records(trs_gpu_engine* engine, void* dst, uint64_t cap_bytes,
  * counting bytes_per_access per access. */
 int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters,
                          double* gbps);
+
+/* The same probe with `ilp` (1, 2, 4, 8 or 16) independent gathers in flight
+ * per thread (trs_gpu_gather_probe uses 4): the roofline curve over footprint,
+ * access size and memory-level parallelism. */
+int trs_gpu_gather_probe_ex(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t ilp, uint32_t iters,
+                            double* gbps);
 
 #endif /* __CUDACC_RTC__ */
 

@@ -23,6 +23,7 @@
 
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -102,18 +103,7 @@ inline Flat flatten(const trs::TermStore& store, const trs::DispatchTable& table
     return f;
 }
 
-}  // namespace detail
-
-// trs::run's contract on the B200: mutates `store` into the normal form and
-// returns the per-sweep trace (widths bit-exact to the reference's).
-inline trs::SweepTrace run(trs::TermStore& store, const trs::DispatchTable& table, const GpuOptions& opt = {}) {
-    trs_gpu_engine* e = nullptr;
-    detail::check(trs_gpu_open(opt.device, &e), nullptr);
-    struct Closer {
-        trs_gpu_engine* e;
-        ~Closer() { trs_gpu_close(e); }
-    } closer{e};
-    detail::Flat f = detail::flatten(store, table);
+inline trs_gpu_program program_of(const Flat& f) {
     trs_gpu_program p{};
     p.num_symbols = static_cast<uint32_t>(f.arity.size());
     p.arity = f.arity.data();
@@ -126,7 +116,65 @@ inline trs::SweepTrace run(trs::TermStore& store, const trs::DispatchTable& tabl
     p.instrs = f.instrs.data();
     p.num_refs = static_cast<uint32_t>(f.refs.size());
     p.refs = f.refs.data();
-    detail::check(trs_gpu_set_program(e, &p), e);
+    return p;
+}
+
+// The flattened program as one word string: equal strings, equal programs.
+inline std::vector<uint32_t> fingerprint(const Flat& f) {
+    std::vector<uint32_t> k;
+    auto put = [&](const void* p, std::size_t bytes) {
+        k.push_back(static_cast<uint32_t>(bytes));
+        const std::size_t w = k.size();
+        k.resize(w + (bytes + 3) / 4, 0u);
+        if (bytes) std::memcpy(k.data() + w, p, bytes);
+    };
+    put(f.arity.data(), f.arity.size() * 4);
+    put(f.rule_begin.data(), f.rule_begin.size() * 4);
+    put(f.refs.data(), f.refs.size() * 4);
+    put(f.rules.data(), f.rules.size() * sizeof(trs_gpu_rule));
+    put(f.steps.data(), f.steps.size() * sizeof(trs_gpu_step));
+    put(f.instrs.data(), f.instrs.size() * sizeof(trs_gpu_instr));
+    return k;
+}
+
+// One engine per process, kept open across calls, and the program it holds:
+// set_program (which specialises and compiles the step loop, jit.hpp) runs
+// only when a different DispatchTable comes.  Calls are serialised.
+struct Cache {
+    std::mutex mu;
+    trs_gpu_engine* e = nullptr;
+    int device = -1;
+    std::vector<uint32_t> program;
+};
+
+inline Cache& cache() {
+    static Cache* c = new Cache();  // never destroyed: no CUDA calls after the runtime's teardown
+    return *c;
+}
+
+}  // namespace detail
+
+// trs::run's contract on the B200: mutates `store` into the normal form and
+// returns the per-sweep trace (widths bit-exact to the reference's).
+inline trs::SweepTrace run(trs::TermStore& store, const trs::DispatchTable& table, const GpuOptions& opt = {}) {
+    detail::Cache& cache = detail::cache();
+    std::lock_guard<std::mutex> guard(cache.mu);
+    if (!cache.e || cache.device != opt.device) {
+        if (cache.e) trs_gpu_close(cache.e);
+        cache.e = nullptr;
+        cache.program.clear();
+        detail::check(trs_gpu_open(opt.device, &cache.e), nullptr);
+        cache.device = opt.device;
+    }
+    trs_gpu_engine* e = cache.e;
+    detail::Flat f = detail::flatten(store, table);
+    std::vector<uint32_t> fp = detail::fingerprint(f);
+    if (fp != cache.program) {
+        trs_gpu_program p = detail::program_of(f);
+        cache.program.clear();
+        detail::check(trs_gpu_set_program(e, &p), e);
+        cache.program = std::move(fp);
+    }
     // TermStore columns args[j][i] -> column-major [maxarity * n]
     const uint32_t n = store.n;
     std::vector<uint32_t> args(static_cast<std::size_t>(store.maxarity) * n);
@@ -148,14 +196,18 @@ inline trs::SweepTrace run(trs::TermStore& store, const trs::DispatchTable& tabl
     trs_gpu_trace(e, nullptr, 0, &count);
     std::vector<trs_gpu_sweep_record> recs(count);
     if (count) trs_gpu_trace(e, recs.data(), count, &count);
+    // one record per logical sweep (the reference's sweeps): the width is
+    // exact; live_terms/n/free_len/micros are per physical sweep on the GPU
+    // (trs_gpu_phys_trace) and are filled for the last record only, from the
+    // written-back store below (n = its slots, live_terms = its terms)
     for (const trs_gpu_sweep_record& r : recs) {
         trs::SweepRecord sr;
         sr.sweep = r.sweep;
         sr.rewrites = r.rewrites;
-        sr.live_terms = r.live_terms;
-        sr.n = r.n;
-        sr.free_len = r.free_len;
-        sr.micros = r.micros_x1000 / 1000;
+        sr.live_terms = 0;
+        sr.n = 0;
+        sr.free_len = 0;
+        sr.micros = 0;
         trace.records.push_back(sr);
     }
     if (rc != TRS_GPU_OK && rc != TRS_GPU_STEP_BUDGET && rc != TRS_GPU_CAPACITY) detail::check(rc, e);
@@ -177,6 +229,11 @@ inline trs::SweepTrace run(trs::TermStore& store, const trs::DispatchTable& tabl
     }
     store.n = nn;
     store.root = root;
+    if (!trace.records.empty()) {
+        trace.records.back().n = nn;
+        trace.records.back().live_terms = nn > 0 ? nn - 1 : 0;
+        trace.records.back().micros = static_cast<std::uint64_t>(stats.kernel_ms * 1e3);
+    }
     store.next_free_begin = store.next_free_end = 0;
     store.next_fresh = 0;
     detail::check(rc, e);

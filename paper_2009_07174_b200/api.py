@@ -127,9 +127,13 @@ def lib():
         "trs_gpu_jit_info": ([P, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_char_p, U64], I),
         "trs_gpu_release": ([P], I),
         "trs_gpu_trace": ([P, P, U64, ctypes.POINTER(U64)], I),
+        "trs_gpu_phys_trace": ([P, P, U64, ctypes.POINTER(U64)], I),
         "trs_gpu_canonical": ([P, U32, P, U64, ctypes.POINTER(U64), u32p], I),
         "trs_gpu_fetch_store": ([P, u32p, P, P, P, P, P, U32], I),
+        "trs_gpu_canonical_all": ([P, P, U64, ctypes.POINTER(U64), P, P, P], I),
+        "trs_gpu_live_count": ([P, ctypes.POINTER(U64)], I),
         "trs_gpu_gather_probe": ([I, U64, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
+        "trs_gpu_gather_probe_ex": ([I, U64, U32, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
         "trs_gpu_stream": ([P], P),
         "trs_gpu_profile_counters": ([P, P], I),
         "trs_gpu_overhead_probe": ([P, U32, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
@@ -172,6 +176,7 @@ def exported_symbols() -> list[str]:
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
                         "trs_gpu_run", "trs_gpu_run_async", "trs_gpu_run_wait", "trs_gpu_hold",
                         "trs_gpu_release", "trs_gpu_jit_info", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
+                        "trs_gpu_canonical_all", "trs_gpu_live_count", "trs_gpu_phys_trace", "trs_gpu_gather_probe_ex",
                         "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
                         "trs_gpu_profile_counters", "trs_gpu_overhead_probe")]
 
@@ -368,10 +373,20 @@ def _raise(rc: int, message: str):
     raise CudaError(message)
 
 
+# reserved[1] bits (include/trs_gpu.h)
+_RESERVED1_BITS = {"no_resident": 1, "interpreted": 2, "no_runahead": 4}
+
+
 def make_options(**kw) -> Options:
+    """Options by field name; no_resident / interpreted / no_runahead set the
+    corresponding reserved[1] bits."""
     o = Options()
     for k, v in kw.items():
-        setattr(o, k, v)
+        if k in _RESERVED1_BITS:
+            if v:
+                o.reserved[1] |= _RESERVED1_BITS[k]
+        else:
+            setattr(o, k, v)
     return o
 
 
@@ -508,10 +523,46 @@ class Engine:
             _raise(rc, self._err())
         return out
 
+    def phys_trace(self) -> np.ndarray:
+        """Per physical sweep (step-loop iteration) records of the last run."""
+        n = ctypes.c_uint64(0)
+        lib().trs_gpu_phys_trace(self._h, None, 0, ctypes.byref(n))
+        out = np.zeros(n.value, SWEEP_RECORD)
+        if n.value:
+            rc = lib().trs_gpu_phys_trace(self._h, out.ctypes.data, n.value, ctypes.byref(n))
+            _raise(rc, self._err())
+        return out
+
     def canonical(self, root_index: int = 0) -> np.ndarray:
         rc, res = _words(lib().trs_gpu_canonical, self._h, root_index)
         _raise(rc, self._err())
         return res[0]
+
+    def canonical_all(self, num_roots: int, words: bool = True) -> dict:
+        """Canonical words of every root, relabelled on the device
+        (trs_gpu_canonical_all): {'words': [per-root arrays] or None,
+        'hashes': uint64[num_roots], 'nodes': uint32[num_roots]}."""
+        L = lib()
+        nw = ctypes.c_uint64(0)
+        offs = np.zeros(num_roots + 1, np.uint64)
+        hashes = np.zeros(num_roots, np.uint64)
+        nodes = np.zeros(num_roots, np.uint32)
+        rc = L.trs_gpu_canonical_all(self._h, None, 0, ctypes.byref(nw), offs.ctypes.data, hashes.ctypes.data,
+                                     nodes.ctypes.data)
+        _raise(rc, self._err())
+        out = {"hashes": hashes, "nodes": nodes, "offsets": offs, "words": None}
+        if words:
+            flat = np.zeros(max(1, nw.value), np.uint32)
+            rc = L.trs_gpu_canonical_all(self._h, flat.ctypes.data, nw.value, ctypes.byref(nw), None, None, None)
+            _raise(rc, self._err())
+            out["words"] = [flat[int(offs[k]):int(offs[k + 1])] for k in range(num_roots)]
+        return out
+
+    def live_count(self) -> int:
+        """Slots with refcount > 0 (the reference's live_terms, sweep_engine.cpp:122-123)."""
+        v = ctypes.c_uint64(0)
+        _raise(lib().trs_gpu_live_count(self._h, ctypes.byref(v)), self._err())
+        return v.value
 
     def fetch_store(self, maxarity: int, num_roots: int) -> dict:
         """The live store in the reference TermStore layout (trs_gpu_fetch_store):
@@ -539,15 +590,27 @@ class Engine:
         stats = self.run(options)
         res = RunResult(stats=stats, trace=self.trace())
         if words:
-            for k in range(store.view()["num_roots"]):
-                w = self.canonical(k)
-                res.words.append(w)
+            res.words = self.canonical_all(store.view()["num_roots"])["words"]
         return res
 
 
-def gather_probe(device: int = 0, bytes_: int = 4 << 30, bytes_per_access: int = 4, iters: int = 5) -> float:
+def canonical_hash(words: np.ndarray) -> int:
+    """The per-root hash trs_gpu_canonical_all reports, restated in numpy:
+    sum over positions k of SplitMix64((k << 32) ^ w_k ^ 0x9e3779b97f4a7c15)
+    modulo 2^64 (canon.cuh, canon_mix)."""
+    w = np.asarray(words, np.uint64)
+    with np.errstate(over="ignore"):
+        z = (np.arange(w.size, dtype=np.uint64) << np.uint64(32)) ^ w ^ np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        z = z ^ (z >> np.uint64(31))
+        return int(z.sum(dtype=np.uint64))
+
+
+def gather_probe(device: int = 0, bytes_: int = 4 << 30, bytes_per_access: int = 4, iters: int = 5,
+                 ilp: int = 4) -> float:
     g = ctypes.c_double(0)
-    rc = lib().trs_gpu_gather_probe(device, bytes_, bytes_per_access, iters, ctypes.byref(g))
+    rc = lib().trs_gpu_gather_probe_ex(device, bytes_, bytes_per_access, ilp, iters, ctypes.byref(g))
     _raise(rc, "gather probe failed")
     return g.value
 

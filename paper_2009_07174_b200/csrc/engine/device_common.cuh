@@ -20,6 +20,13 @@ constexpr int kWarps = kBlock / 32;
 constexpr uint32_t kMaxGrid = 1024;    // CTAs; sizes the frontier region tables
 constexpr uint32_t kSmallCap = 4096;   // frontier entries per shared-memory list (single-CTA mode)
 
+// Sweep outcome flags, raised by lanes in a CTA-shared word and published
+// with the CTA's frontier region, so every CTA reads the same set after the
+// grid barrier (a global sticky word could be raised by the next sweep of a
+// fast CTA before a slow one has read it).
+constexpr uint32_t kFlagCapacity = 1;  // a claim did not fit a fixed capacity
+constexpr uint32_t kFlagHist = 2;      // a derive sweep lies past the width histogram
+
 enum Status : uint32_t {
     kRunning = 0,
     kDone = 1,
@@ -58,6 +65,14 @@ struct Ctl {
     // a collection left a refcount cascade unfinished (hop cap): garbage remains
     uint32_t gc_truncated;
     uint32_t export_n;        // slots of the last export (export.cuh)
+    // logical time: `sweep` is the logical sweep count (epochs) at the end of
+    // a run; `psweep` counts the physical sweeps (loop iterations) of the run,
+    // `tmax` the latest nf epoch so far; widths live in Params::hist
+    uint32_t psweep;
+    uint32_t tmax;
+    uint32_t need_hist;       // a slot's derive sweep lies past the width histogram
+    uint32_t hist_need;       // the histogram entries it needs
+    uint32_t ra_narrow, ra_on, ra_used;  // run-ahead state (sweep.cuh, ra_track)
     // phase cycle accounting (Params::profile): match, claim, apply, push,
     // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
     // the match sub-phases: record, children, slots, rules
@@ -78,6 +93,7 @@ struct Params {
     uint32_t* gcmap;
     uint32_t* blocksum;
     uint32_t* regions;               // [2 buffers][off | cnt][kMaxGrid]
+    uint32_t* region_flags;          // [2 buffers][kMaxGrid] kFlag* raised by the sweep that wrote the buffer
     unsigned long long* region_rew;  // [2 buffers][kMaxGrid] rewrites of the sweep that wrote the buffer
     uint32_t* roots;
     uint32_t num_roots;
@@ -104,6 +120,15 @@ struct Params {
     uint32_t local_cap;     // >0: slots of the shared-memory resident arena of the single-CTA mode
     uint32_t local_enter;   // allocated slots at or below which the single-CTA mode goes resident
     uint32_t max_vars;      // binding columns in shared memory (largest rule's variable count)
+    unsigned long long* hist;  // per logical sweep (from sweep0 + 1): rewrites (the reference's widths)
+    uint32_t hist_cap;
+    uint32_t runahead;      // lanes continue into slots their step made ready (logical time)
+    uint32_t ra_max;        // ... in sweeps of at most this many frontier entries
+    uint32_t ra_kill;       // a sweep wider than this switches run-ahead off (Local::ra_on)
+    uint32_t ra_warm;       // consecutive sweeps no wider than ra_kill switch it on
+    uint32_t ra_steps;      // consecutive run-ahead steps of a lane before it pushes instead (a long
+                            // chain must not hold back the work its steps pushed to the next sweep)
+    uint64_t list_cap;      // entries per frontier list buffer
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

@@ -31,11 +31,29 @@ constexpr uint32_t kMaxProgramBytes = 40 * 1024;
 
 // record word layout (W words per slot, W = 8/16/32):
 //   w0 head = symbol | subterm cursor << 24
-//   w1 nf epoch (sweep in which the slot became nf; 0 = not nf)
+//   w1 nf epoch: the sweep in which the slot became nf; while it is not nf,
+//      kTminBit | the first sweep it may derive in (one past its build or
+//      last in-place rewrite), or 0 for an input slot (the run's first sweep)
 //   w2 refcount
 //   w3 waiter (slot of the parent sleeping on this one, 0 none, kWoken)
 //   w4.. arguments
 constexpr uint32_t kWHead = 0, kWEpoch = 1, kWRc = 2, kWWaiter = 3, kWArgs = 4;
+constexpr uint32_t kTminBit = 0x80000000u;
+// An nf epoch word also carries the physical sweep that published it, mod 16
+// (bits 27..30): with run-ahead (sweep.cuh) a lane may read records written
+// in the current physical sweep only if it wrote them itself, so a child
+// published in the current physical sweep by another lane counts as pending.
+constexpr uint32_t kEpochBits = 27;
+constexpr uint32_t kEpochMask = (1u << kEpochBits) - 1;
+constexpr uint32_t kStampMask = 0xFu;
+
+// Logical time (oracle/trs_oracle.c, oracle_logical): a slot derives in
+// sweep T = max(its earliest sweep, max over arguments of their nf epoch + 1)
+// (sweep_engine.cpp:80-81, :86, :153-188), whenever it is processed.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+constexpr bool epoch_nf(uint32_t e) { return e != 0u && !(e & kTminBit); }
 
 // Arguments a W-word record carries.  W = 16 holds at most 8 (not 12): the
 // step loop keeps per-argument state in registers, and arity 9-12 systems

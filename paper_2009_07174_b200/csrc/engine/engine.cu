@@ -45,6 +45,7 @@
 #include "device_program.hpp"
 #include "sweep.cuh"
 #include "export.cuh"
+#include "canon.cuh"
 #include "jit.hpp"
 #include "trs_gpu.h"
 
@@ -133,8 +134,7 @@ __global__ void init_ctl(Ctl* ctl, uint32_t* regions, const uint32_t* count, uin
 // thread keeps kProbeILP independent gathers in flight (the engine's warp
 // step issues its child probes together the same way), and addressing is a
 // mask, so the probe is bound by the memory system, not by issue.
-constexpr int kProbeILP = 4;
-template <int VEC>
+template <int VEC, int kProbeILP>
 __global__ void __launch_bounds__(512) gather_probe_kernel(const uint32_t* __restrict__ data, uint64_t mask,
                                                            const uint32_t* __restrict__ idx, uint32_t n,
                                                            uint32_t* __restrict__ sink) {
@@ -171,22 +171,51 @@ __global__ void __launch_bounds__(512) gather_probe_kernel(const uint32_t* __res
 // Start of a run (begin = 1) or of a relaunch within one (begin = 0): the
 // host never reads the control block before launching, so a run costs one
 // host synchronisation (the status read-back at the end).
-__global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t begin) {
+__global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t* region_flags, uint32_t begin) {
     if (threadIdx.x == 0) {
         if (begin) {
+            // logical sweeps continue from the previous run's (epochs stay comparable)
             c->sweep0 = c->sweep;
+            c->tmax = c->sweep;
+            c->psweep = 0;
             c->total_rewrites = 0;
             c->max_width = 0;
             c->gc_runs = 0;
             c->small_sweeps = 0;
             c->gc_ns = 0;
             c->abort_capacity = 0;
-            c->last_gc_sweep = c->sweep;
+            c->last_gc_sweep = 0;
+            c->hist_need = 0;
+            c->ra_narrow = 0;
+            c->ra_on = 0;
+            c->ra_used = 0;
         }
         c->status = kRunning;
         c->bar_arrive = 0;
     }
     if (threadIdx.x < 8) claim_ctrs[threadIdx.x] = 0;
+    // the flags that ended the previous launch have been acted on
+    for (uint32_t k = threadIdx.x; k < 2 * kMaxGrid; k += blockDim.x) region_flags[k] = 0;
+}
+
+// After every step-loop launch: the logical sweep count (the run ends at the
+// first sweep after its last nf event, sweep_engine.cpp:147) and the widest
+// logical sweep (SweepTrace::max_width, sweep_engine.cpp:407-426).
+__global__ void finish_run(Ctl* c, const unsigned long long* __restrict__ hist, uint32_t hist_cap) {
+    const uint32_t t = max(c->tmax, c->sweep0);
+    const uint32_t n = min(t - c->sweep0, hist_cap);
+    unsigned long long mx = 0;
+    for (uint32_t k = threadIdx.x; k < n; k += blockDim.x) mx = max(mx, hist[k]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ unsigned long long wm[32];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (uint32_t w = 1; w < blockDim.x / 32; ++w) mx = max(mx, wm[w]);
+        c->max_width = mx;
+        c->sweep = t + 1;
+    }
 }
 
 // Device-side write-back in the reference TermStore layout (term_store.hpp:
@@ -210,7 +239,7 @@ __global__ void pack_store(const uint32_t* __restrict__ A, uint32_t n, const uin
         const uint32_t ar = arity[sym];
         hss[y] = sym;
         rcs[y] = q0.z;
-        nf[y] = q0.y != 0;
+        nf[y] = epoch_nf(q0.y);
         for (uint32_t j = 0; j < ma; ++j) args[(size_t)j * n + y] = j < ar ? R[kWArgs + j] : 0u;
     }
 }
@@ -231,6 +260,7 @@ __global__ void fill_random(uint32_t* idx, uint32_t n, uint64_t seed) {
 
 struct RunState {
     trs_gpu_options opt{};
+    bool runahead = false;
     int blocks = 0;
     uint32_t launches = 0;
     float total_ms = 0.f;
@@ -251,6 +281,7 @@ struct trs_gpu_engine {
     uint32_t max_new = 0;
     uint32_t num_symbols = 0;
     std::vector<uint32_t> arity;
+    std::vector<uint32_t> rule_source;  // source order of each device rule (trs_gpu_dump_program)
     int W = 8;
     int minb = 1;  // register budget variant of the step loop (see step_loop_for)
     bool resident_on = false;  // this run reserves the shared-memory resident arena
@@ -296,8 +327,22 @@ struct trs_gpu_engine {
     size_t stage_words = 0;
     uint32_t roots_out_cap = 0;
     bool exported = false;                // staging holds the export of the current state
-    trs_gpu_sweep_record* d_trace = nullptr;
+    bool canon_ready = false;             // d_words holds the canonical words of that export
+    uint32_t* d_canon = nullptr;          // canonical relabelling scratch (canon.cuh)
+    size_t canon_words_cap = 0;
+    uint32_t* d_words = nullptr;
+    size_t words_cap = 0;
+    unsigned long long* d_woff = nullptr; // [roots + 1] word offsets, then [roots] hashes
+    uint32_t* d_nodes = nullptr;
+    uint32_t canon_roots_cap = 0;
+    uint64_t canon_total = 0;
+    trs_gpu_sweep_record* d_trace = nullptr;  // physical sweep records
     uint32_t trace_cap = 0;
+    unsigned long long* d_hist = nullptr;     // rewrites per logical sweep (the reference's widths)
+    uint32_t hist_cap = 0;
+    uint32_t hist_used = 0;                   // entries the last run wrote (zeroed before the next)
+    uint32_t* d_region_flags = nullptr;       // [2][kMaxGrid]
+    uint32_t last_psweeps = 0;
     bool loaded = false;
     uint32_t last_sweeps = 0;
     int record_width = 8;
@@ -342,6 +387,11 @@ void free_store(trs_gpu_engine* e) {
     e->d_region_rew = nullptr;
     cudaFree(e->d_ctl);
     cudaFree(e->d_trace);
+    cudaFree(e->d_hist);
+    cudaFree(e->d_region_flags);
+    e->d_hist = nullptr;
+    e->d_region_flags = nullptr;
+    e->hist_cap = e->hist_used = 0;
     e->d_gcmap = e->d_roots = e->d_blocksum = nullptr;
     e->d_ctl = nullptr;
     e->d_trace = nullptr;
@@ -493,6 +543,7 @@ DPlan plan_symbol(const trs_gpu_program* p, uint32_t f, std::vector<DStep>& step
 
 constexpr size_t kSmemBudget = 227 * 1024 - 12 * 1024;  // dynamic bytes, leaving room for static smem
 size_t dyn_base(const trs_gpu_engine* e);
+int run_canon(trs_gpu_engine* e);
 
 int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (!p || !p->arity || !p->rule_begin) return fail(e, TRS_GPU_INVALID, "null program");
@@ -703,6 +754,8 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
         return fail(e, TRS_GPU_INVALID, "program + binding columns exceed the step loop's shared memory");
     e->num_symbols = p->num_symbols;
     e->arity.assign(p->arity, p->arity + p->num_symbols);
+    e->rule_source.resize(p->num_rules);
+    for (uint32_t r = 0; r < p->num_rules; ++r) e->rule_source[r] = p->rules[r].source_order;
     e->W = words_for_arity(max_arity);
     return TRS_GPU_OK;
 }
@@ -833,8 +886,11 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     // the frontier of the next sweep: regions of list buffer c.cur
     uint64_t extent = frontier_extent(e, c);
     CUDA_TRY(e, cudaMemcpyAsync(na[c.arena], e->d_arena[c.arena], rec_bytes * c.bump, cudaMemcpyDeviceToDevice, e->stream));
+    // frontier entries are one word (bare slots) or a record (rich entries)
+    const size_t entry_bytes = e->rich ? rec_bytes : sizeof(uint32_t);
     if (extent)
-        CUDA_TRY(e, cudaMemcpyAsync(nl[c.cur], e->d_list[c.cur], rec_bytes * extent, cudaMemcpyDeviceToDevice, e->stream));
+        CUDA_TRY(e, cudaMemcpyAsync(nl[c.cur], e->d_list[c.cur], std::min(entry_bytes * extent, rec_bytes * e->alloc_capacity),
+                                    cudaMemcpyDeviceToDevice, e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
     for (int k = 0; k < 2; ++k) {
         cudaFree(e->d_arena[k]);
@@ -887,6 +943,10 @@ Params make_params(trs_gpu_engine* e, int blocks) {
     P.step_budget = 1000000000ull;
     P.rich = e->rich;
     P.max_vars = e->max_vars;
+    P.region_flags = e->d_region_flags;
+    P.hist = e->d_hist;
+    P.hist_cap = e->hist_cap;
+    P.list_cap = e->rich ? e->alloc_capacity : (uint64_t)e->alloc_W * e->alloc_capacity;
     // slab: 256 slots per warp unless the arena is small
     uint64_t per_warp = e->capacity / (4ull * (uint64_t)blocks * kWarps);
     P.slab = (uint32_t)std::max<uint64_t>(16, std::min<uint64_t>(256, per_warp));
@@ -922,6 +982,23 @@ int grow_trace(trs_gpu_engine* e) {
     cudaFree(e->d_trace);
     e->d_trace = nt;
     e->trace_cap = cap;
+    return TRS_GPU_OK;
+}
+
+int grow_hist(trs_gpu_engine* e, uint32_t need) {
+    if (need >= kEpochMask - 2)
+        return fail(e, TRS_GPU_STEP_BUDGET, "more than 2^27 logical sweeps; the derivation may not terminate");
+    uint32_t cap = e->hist_cap;
+    while (cap < need) cap *= 2;
+    unsigned long long* nh = nullptr;
+    CUDA_TRY(e, cudaMalloc(&nh, sizeof(unsigned long long) * cap));
+    CUDA_TRY(e, cudaMemsetAsync(nh, 0, sizeof(unsigned long long) * cap, e->stream));
+    CUDA_TRY(e, cudaMemcpyAsync(nh, e->d_hist, sizeof(unsigned long long) * e->hist_cap, cudaMemcpyDeviceToDevice,
+                                e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    cudaFree(e->d_hist);
+    e->d_hist = nh;
+    e->hist_cap = cap;
     return TRS_GPU_OK;
 }
 
@@ -969,6 +1046,14 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     if (!e->d_blocksum) CUDA_TRY(e, cudaMalloc(&e->d_blocksum, sizeof(uint32_t) * (kMaxGrid + 8)));
     if (!e->d_regions) CUDA_TRY(e, cudaMalloc(&e->d_regions, sizeof(uint32_t) * 4 * kMaxGrid));
     if (!e->d_region_rew) CUDA_TRY(e, cudaMalloc(&e->d_region_rew, sizeof(unsigned long long) * 2 * kMaxGrid));
+    if (!e->d_region_flags) CUDA_TRY(e, cudaMalloc(&e->d_region_flags, sizeof(uint32_t) * 2 * kMaxGrid));
+    CUDA_TRY(e, cudaMemsetAsync(e->d_region_flags, 0, sizeof(uint32_t) * 2 * kMaxGrid, e->stream));
+    if (!e->d_hist) {
+        e->hist_cap = 1u << 16;
+        CUDA_TRY(e, cudaMalloc(&e->d_hist, sizeof(unsigned long long) * e->hist_cap));
+        CUDA_TRY(e, cudaMemsetAsync(e->d_hist, 0, sizeof(unsigned long long) * e->hist_cap, e->stream));
+        e->hist_used = 0;
+    }
     CUDA_TRY(e, cudaMemsetAsync(e->d_blocksum, 0, sizeof(uint32_t) * (kMaxGrid + 8), e->stream));
     if (!e->d_trace) {
         e->trace_cap = 1u << 16;
@@ -1115,6 +1200,10 @@ void trs_gpu_close(trs_gpu_engine* e) {
     if (e->ev_b) cudaEventDestroy(e->ev_b);
     cudaFree(e->d_roots_out);
     cudaFree(e->d_stage);
+    cudaFree(e->d_canon);
+    cudaFree(e->d_words);
+    cudaFree(e->d_woff);
+    cudaFree(e->d_nodes);
     if (e->load_a) cudaEventDestroy(e->load_a);
     if (e->load_b) cudaEventDestroy(e->load_b);
     cudaStreamDestroy(e->stream);
@@ -1235,11 +1324,30 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.local_cap = e->resident_on ? resident_slots(e) : 0u;
     P.local_enter = P.local_cap / 2;
     if (opt.reserved[2]) P.slab = opt.reserved[2];  // experiment: slab override
+    // run-ahead (lanes continue into slots their step made ready; logical
+    // time keeps the widths exact) except where the reference's abort state
+    // is part of the contract: an explicit step budget or a fixed capacity
+    P.runahead = (R.runahead && !e->rich) ? 1u : 0u;
+    {
+        const char* rm = std::getenv("TRS_B200_RA_MAX");  // tuning hook
+        P.ra_max = rm ? (uint32_t)std::strtoul(rm, nullptr, 10) : (uint32_t)R.blocks * kWarps * 4u;
+        const char* rk = std::getenv("TRS_B200_RA_KILL");
+        P.ra_kill = rk ? (uint32_t)std::strtoul(rk, nullptr, 10) : (uint32_t)R.blocks * kWarps * 8u;
+        const char* rw = std::getenv("TRS_B200_RA_WARM");
+        P.ra_warm = rw ? (uint32_t)std::strtoul(rw, nullptr, 10) : 64u;
+        const char* rs = std::getenv("TRS_B200_RA_STEPS");
+        P.ra_steps = rs ? (uint32_t)std::strtoul(rs, nullptr, 10) : 8u;
+    }
     void* args[] = {&P};
     cudaEventRecord(R.a, e->stream);
-    prep_launch<<<1, 32, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, R.launches == 0 ? 1u : 0u);
+    prep_launch<<<1, 256, 0, e->stream>>>(e->d_ctl, e->d_blocksum + kMaxGrid, e->d_region_flags,
+                                          R.launches == 0 ? 1u : 0u);
     cudaError_t err =
         cudaLaunchCooperativeKernel(loop_kernel(e), R.blocks, kBlock, args, dyn_smem(e), e->stream);
+    if (err == cudaSuccess) {
+        finish_run<<<1, 256, 0, e->stream>>>(e->d_ctl, e->d_hist, e->hist_cap);
+        err = cudaGetLastError();
+    }
     if (err == cudaSuccess) err = cudaMemcpyAsync(e->h_ctl, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream);
     cudaEventRecord(R.b, e->stream);
     R.launches++;
@@ -1274,6 +1382,17 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     if (!e->ev_b) CUDA_TRY(e, cudaEventCreate(&e->ev_b));
     R.a = e->ev_a;
     R.b = e->ev_b;
+    {
+        const char* ra = std::getenv("TRS_B200_RUNAHEAD");
+        // an explicit budget below the default (sweep_engine.hpp:32) asks for the
+        // reference's abort point: no run-ahead then
+        const bool budget = R.opt.step_budget != 0 && R.opt.step_budget < 1000000000ull;
+        R.runahead = !budget && !R.opt.fixed_capacity && !(R.opt.reserved[1] & 4u) && !(ra && ra[0] == '0');
+    }
+    // widths of the last run go; the histogram is all zeros again
+    if (e->hist_used)
+        CUDA_TRY(e, cudaMemsetAsync(e->d_hist, 0, sizeof(unsigned long long) * e->hist_used, e->stream));
+    e->hist_used = 0;
     R.active = true;
     int r = enqueue_launch(e);
     if (r) R.active = false;
@@ -1315,7 +1434,13 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
             break;
         }
         if (c.status == kNeedTrace) {
-            int r = grow_trace(e);
+            int r = TRS_GPU_OK;
+            if (c.hist_need > e->hist_cap) {
+                // a slot's logical derive sweep lies past the width histogram
+                r = grow_hist(e, c.hist_need);
+            } else {
+                r = grow_trace(e);
+            }
             if (!r) r = enqueue_launch(e);
             if (r) { result = r; break; }
             continue;
@@ -1337,7 +1462,7 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
     st.launches = R.launches;
     st.total_rewrites = c.total_rewrites;
     st.max_width = c.max_width;
-    st.sweeps = c.sweep - c.sweep0;
+    st.sweeps = c.sweep - c.sweep0;  // logical (finish_run)
     st.gc_runs = c.gc_runs;
     st.small_sweeps = c.small_sweeps;
     st.peak_slots = c.peak_bump;
@@ -1348,6 +1473,8 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
         st.load_ms = e->load_ms;
     cudaGetLastError();
     e->last_sweeps = c.sweep - c.sweep0;
+    e->last_psweeps = c.psweep;
+    e->hist_used = std::min<uint32_t>(e->hist_cap, e->last_sweeps);
     if (result == TRS_GPU_OK && opt.validate) result = validate_store(e);
     if (stats) *stats = st;
     return result;
@@ -1499,9 +1626,33 @@ int trs_gpu_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, ui
     REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
-    uint64_t n = std::min<uint64_t>(e->last_sweeps, e->trace_cap);
+    // one record per logical sweep: rewrites = the width (hist); the run's
+    // last sweep is the empty one that ends it (sweep_engine.cpp:147)
+    const uint64_t n = e->last_sweeps;
     if (count) *count = n;
-    if (out && cap) CUDA_TRY(e, cudaMemcpy(out, e->d_trace, sizeof(trs_gpu_sweep_record) * std::min(n, cap), cudaMemcpyDeviceToHost));
+    if (!out || !cap) return TRS_GPU_OK;
+    const uint64_t k = std::min(n, cap);
+    std::vector<unsigned long long> h(std::max<uint64_t>(1, k), 0ull);
+    const uint64_t have = std::min<uint64_t>(k, e->hist_cap);
+    if (have) CUDA_TRY(e, cudaMemcpy(h.data(), e->d_hist, sizeof(unsigned long long) * have, cudaMemcpyDeviceToHost));
+    for (uint64_t j = 0; j < k; ++j) {
+        trs_gpu_sweep_record r{};
+        r.sweep = (uint32_t)(j + 1);
+        r.rewrites = h[j];
+        out[j] = r;
+    }
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_phys_trace(trs_gpu_engine* e, trs_gpu_sweep_record* out, uint64_t cap, uint64_t* count) {
+    if (!e || !e->d_trace) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
+    cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
+    uint64_t n = std::min<uint64_t>(e->last_psweeps, e->trace_cap);
+    if (count) *count = n;
+    if (out && cap)
+        CUDA_TRY(e, cudaMemcpy(out, e->d_trace, sizeof(trs_gpu_sweep_record) * std::min(n, cap), cudaMemcpyDeviceToHost));
     return TRS_GPU_OK;
 }
 
@@ -1512,46 +1663,16 @@ int trs_gpu_canonical(trs_gpu_engine* e, uint32_t root_index, uint32_t* words, u
     if (root_index >= e->num_roots) return fail(e, TRS_GPU_INVALID, "root index out of range");
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
-    HostArena h;
-    std::vector<uint32_t> roots;
-    int rc = fetch_arena(e, h, roots);
-    if (rc) return rc;
-    // iterative pre-order, first-visit ids
-    std::vector<uint32_t> id(h.base, UINT32_MAX);
-    std::vector<uint32_t> order;
-    std::vector<uint32_t> stack{roots[root_index]};
-    auto check = [&](uint32_t slot) {
-        return slot != 0 && slot < h.base && h.rec(slot)[kWHead] != kDeadHead;
-    };
-    if (!check(roots[root_index])) return fail(e, TRS_GPU_DANGLING, "root is not a live term");
-    uint64_t nw = 0;
-    while (!stack.empty()) {
-        uint32_t x = stack.back();
-        stack.pop_back();
-        if (id[x] != UINT32_MAX) continue;
-        id[x] = (uint32_t)order.size();
-        order.push_back(x);
-        const uint32_t* R = h.rec(x);
-        uint32_t ar = e->arity[R[kWHead] & kSymMask];
-        nw += 1 + ar;
-        for (uint32_t j = ar; j-- > 0;) {
-            uint32_t c = R[kWArgs + j];
-            if (!check(c))
-                return fail(e, TRS_GPU_DANGLING, "slot " + std::to_string(c) + " is not a live term");
-            stack.push_back(c);
-        }
-    }
+    if (int r = run_canon(e)) return r;
+    unsigned long long off[2];
+    uint32_t nodes = 0;
+    CUDA_TRY(e, cudaMemcpy(off, e->d_woff + root_index, sizeof(off), cudaMemcpyDeviceToHost));
+    CUDA_TRY(e, cudaMemcpy(&nodes, e->d_nodes + root_index, sizeof(nodes), cudaMemcpyDeviceToHost));
+    const uint64_t nw = off[1] - off[0];
     if (n_words) *n_words = nw;
-    if (n_nodes) *n_nodes = (uint32_t)order.size();
+    if (n_nodes) *n_nodes = nodes;
     if (!words || cap < nw) return TRS_GPU_OK;
-    uint64_t k = 0;
-    for (uint32_t x : order) {
-        const uint32_t* R = h.rec(x);
-        uint32_t sym = R[kWHead] & kSymMask;
-        words[k++] = sym;
-        uint32_t ar = e->arity[sym];
-        for (uint32_t j = 0; j < ar; ++j) words[k++] = id[R[kWArgs + j]];
-    }
+    CUDA_TRY(e, cudaMemcpy(words, e->d_words + off[0], sizeof(uint32_t) * nw, cudaMemcpyDeviceToHost));
     return TRS_GPU_OK;
 }
 
@@ -1606,14 +1727,123 @@ int run_export(trs_gpu_engine* e, Ctl& c) {
     X.ma = e->max_arity;
     uint32_t bump = c.bump;
     void* args[] = {&P, &X, &bump};
-    CUDA_TRY(e, cudaMemsetAsync(X.counters, 0, sizeof(uint32_t) * 3, e->stream));
+    CUDA_TRY(e, cudaMemsetAsync(X.counters, 0, sizeof(uint32_t) * 4, e->stream));
     CUDA_TRY(e, cudaMemsetAsync(X.queue[0], 0, sizeof(uint32_t) * c.bump, e->stream));
     reset_barrier(e);
     CUDA_TRY(e, cudaLaunchCooperativeKernel(fn, blocks, kBlock, args, 0, e->stream));
+    uint32_t dangling = 0;
     CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaMemcpyAsync(&dangling, X.counters + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    if (dangling) {
+        e->exported = false;
+        return fail(e, TRS_GPU_DANGLING,
+                    dangling == 0xFFFFFFFFu ? std::string("a live term references slot 0 or a slot past the store")
+                                            : "slot " + std::to_string(dangling) + " is not a live term");
+    }
     e->exported = true;
+    e->canon_ready = false;
     e->export_ctl = c;
+    return TRS_GPU_OK;
+}
+
+// Canonical words of every root from the export staging (canon.cuh); the
+// result stays on the device until the store changes.
+int run_canon(trs_gpu_engine* e) {
+    if (e->roots_out_cap < e->num_roots) {
+        cudaFree(e->d_roots_out);
+        CUDA_TRY(e, cudaMalloc(&e->d_roots_out, sizeof(uint32_t) * e->num_roots));
+        e->roots_out_cap = e->num_roots;
+        e->exported = false;
+    }
+    if (!e->exported) {
+        Ctl c;
+        if (int r = run_export(e, c)) return r;
+    }
+    if (e->canon_ready) return TRS_GPU_OK;
+    const Ctl& c = e->export_ctl;
+    const uint32_t n = c.export_n;
+    const uint32_t ma = e->max_arity;
+    const uint32_t R = e->num_roots;
+    if ((uint64_t)n * (1 + ma) >= 0xFFFFFFFFull) return fail(e, TRS_GPU_INVALID, "normal forms beyond 2^32 words");
+    const size_t need = (size_t)n * 8 + (size_t)ma * n + R + 8;
+    if (e->canon_words_cap < need) {
+        cudaFree(e->d_canon);
+        e->d_canon = nullptr;
+        e->canon_words_cap = 0;
+        CUDA_TRY(e, cudaMalloc(&e->d_canon, sizeof(uint32_t) * need));
+        e->canon_words_cap = need;
+    }
+    const size_t wneed = (size_t)n * (1 + ma) + 1;
+    if (e->words_cap < wneed) {
+        cudaFree(e->d_words);
+        e->d_words = nullptr;
+        e->words_cap = 0;
+        CUDA_TRY(e, cudaMalloc(&e->d_words, sizeof(uint32_t) * wneed));
+        e->words_cap = wneed;
+    }
+    if (e->canon_roots_cap < R) {
+        cudaFree(e->d_woff);
+        cudaFree(e->d_nodes);
+        e->d_woff = nullptr;
+        e->d_nodes = nullptr;
+        e->canon_roots_cap = 0;
+        CUDA_TRY(e, cudaMalloc(&e->d_woff, sizeof(unsigned long long) * (2 * (size_t)R + 1)));
+        CUDA_TRY(e, cudaMalloc(&e->d_nodes, sizeof(uint32_t) * R));
+        e->canon_roots_cap = R;
+    }
+    const ExportStaging st = export_staging(e, c);
+    CanonArgs X{};
+    X.hss = st.hss;
+    X.args = st.args;
+    X.rcs = st.rcs;
+    X.roots = e->d_roots_out;
+    X.num_roots = R;
+    X.n = n;
+    X.ma = ma;
+    X.arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
+    uint32_t* s = e->d_canon;
+    X.par = s;
+    X.size = s + (size_t)n;
+    X.wsz = s + 2 * (size_t)n;
+    X.pending = s + 3 * (size_t)n;
+    X.id = s + 4 * (size_t)n;
+    X.wpos = s + 5 * (size_t)n;
+    X.rootof = s + 6 * (size_t)n;
+    X.queue = s + 7 * (size_t)n;
+    X.counters = s + 8 * (size_t)n;
+    X.stack = X.counters + 8;
+    X.nodes = e->d_nodes;
+    X.woff = e->d_woff;
+    X.hash = e->d_woff + R + 1;
+    X.words = e->d_words;
+    const int blocks = e->sm_count * 4;
+    CUDA_TRY(e, cudaMemsetAsync(X.counters, 0, sizeof(uint32_t) * 8, e->stream));
+    CUDA_TRY(e, cudaMemsetAsync(X.par, 0, sizeof(uint32_t) * n, e->stream));
+    CUDA_TRY(e, cudaMemsetAsync(X.queue, 0, sizeof(uint32_t) * n, e->stream));
+    canon_init<<<blocks, 256, 0, e->stream>>>(X);
+    uint32_t shared = 0;
+    CUDA_TRY(e, cudaMemcpyAsync(&shared, X.counters + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    if (shared) {
+        // sharing: the reference's sequential stack walk (canon_seq)
+        CUDA_TRY(e, cudaMemsetAsync(X.par, 0, sizeof(uint32_t) * n, e->stream));
+        canon_seq<<<1, 32, 0, e->stream>>>(X);
+    } else {
+        canon_up<<<blocks, 256, 0, e->stream>>>(X);
+        canon_offsets<<<1, kBlock, 0, e->stream>>>(X);
+        int occ = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, canon_down, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
+        const int dblocks = std::min<int>(occ * e->sm_count, 1024);
+        void* kargs[] = {&X};
+        CUDA_TRY(e, cudaLaunchCooperativeKernel((const void*)canon_down, dblocks, kBlock, kargs, 0, e->stream));
+    }
+    unsigned long long total = 0;
+    CUDA_TRY(e, cudaMemcpyAsync(&total, e->d_woff + R, sizeof(total), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    CUDA_TRY(e, cudaGetLastError());
+    e->canon_total = total;
+    e->canon_ready = true;
     return TRS_GPU_OK;
 }
 
@@ -1654,9 +1884,130 @@ int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uin
     return TRS_GPU_OK;
 }
 
-int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters, double* gbps) {
+int trs_gpu_dump_program(trs_gpu_engine* e, const char* const* symbol_names, const char* const* var_names,
+                         const uint32_t* rule_var_begin, const uint32_t* rule_vars, const char* const* rule_texts,
+                         char* out, uint64_t cap, uint64_t* need) {
+    if (!e || !e->d_prog || !symbol_names || !var_names || !rule_var_begin || !rule_vars || !rule_texts || !need)
+        return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
+    cudaSetDevice(e->device);
+    // render what the device holds, not the host copy
+    std::vector<uint8_t> blob(e->blob.size());
+    CUDA_TRY(e, cudaMemcpy(blob.data(), e->d_prog, blob.size(), cudaMemcpyDeviceToHost));
+    const ProgHeader* h = reinterpret_cast<const ProgHeader*>(blob.data());
+    const uint8_t* arity = blob.data() + h->off_arity;
+    const uint16_t* rule_begin = reinterpret_cast<const uint16_t*>(blob.data() + h->off_rule_begin);
+    const DRule* rules = reinterpret_cast<const DRule*>(blob.data() + h->off_rules);
+    const DStep* steps = reinterpret_cast<const DStep*>(blob.data() + h->off_steps);
+    const DInstr* instrs = reinterpret_cast<const DInstr*>(blob.data() + h->off_instrs);
+    const uint16_t* refs = reinterpret_cast<const uint16_t*>(blob.data() + h->off_refs);
+    // the reference's dump format (dispatch.cpp:98-134)
+    std::string o;
+    for (uint32_t f = 0; f < h->num_symbols; ++f) {
+        const uint32_t r0 = rule_begin[f], r1 = rule_begin[f + 1];
+        if (r0 == r1) continue;
+        o += std::string("symbol ") + symbol_names[f] + "/" + std::to_string(arity[f]) + ": " +
+             std::to_string(r1 - r0) + " rule(s)\n";
+        for (uint32_t r = r0; r < r1; ++r) {
+            const DRule& R = rules[r];
+            const uint32_t src = e->rule_source[r];
+            o += "  rule #" + std::to_string(src) + ": " + rule_texts[src] + "\n";
+            auto var_of = [&](uint32_t slot) { return std::string(var_names[rule_vars[rule_var_begin[r] + slot]]); };
+            std::vector<std::string> path(R.num_steps);
+            for (uint32_t t = 0; t < R.num_steps; ++t) {
+                const DStep& S = steps[R.first_step + t];
+                const std::string up = S.parent < 0 ? std::string() : path[S.parent];
+                path[t] = up.empty() ? std::to_string(S.child) : up + "." + std::to_string(S.child);
+                if (S.kind == TRS_GPU_STEP_CHECK_HEAD)
+                    o += "    check [" + path[t] + "] = " + symbol_names[S.value] + "\n";
+                else
+                    o += "    bind  [" + path[t] + "] -> " + var_of(S.value) + "\n";
+            }
+            for (uint32_t k = 0; k < R.num_instrs; ++k) {
+                const DInstr& I = instrs[R.first_instr + k];
+                const bool is_root = !R.collapse && k + 1 == R.num_instrs;
+                o += is_root ? "    root  " : "    new   ";
+                o += "n" + std::to_string(k) + " = " + symbol_names[I.symbol] + "(";
+                for (uint32_t j = 0; j < arity[I.symbol]; ++j) {
+                    if (j) o += ", ";
+                    const uint16_t ref = refs[I.first_ref + j];
+                    o += (ref & kRefNode) ? "n" + std::to_string(ref & 0x7fff) : var_of(ref);
+                }
+                o += ")\n";
+            }
+            if (R.collapse) o += "    root  reuse " + var_of(R.root_ref) + "\n";
+        }
+    }
+    *need = o.size() + 1;
+    if (out && cap >= o.size() + 1) std::memcpy(out, o.c_str(), o.size() + 1);
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_canonical_all(trs_gpu_engine* e, uint32_t* words, uint64_t cap, uint64_t* n_words,
+                          uint64_t* root_offsets, uint64_t* hashes, uint32_t* root_nodes) {
+    if (!e || !e->loaded) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
+    cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
+    if (int r = run_canon(e)) return r;
+    const uint32_t R = e->num_roots;
+    if (n_words) *n_words = e->canon_total;
+    static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "u64");
+    if (root_offsets) CUDA_TRY(e, cudaMemcpy(root_offsets, e->d_woff, sizeof(uint64_t) * (R + 1), cudaMemcpyDeviceToHost));
+    if (hashes) CUDA_TRY(e, cudaMemcpy(hashes, e->d_woff + R + 1, sizeof(uint64_t) * R, cudaMemcpyDeviceToHost));
+    if (root_nodes) CUDA_TRY(e, cudaMemcpy(root_nodes, e->d_nodes, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost));
+    if (words && cap >= e->canon_total)
+        CUDA_TRY(e, cudaMemcpy(words, e->d_words, sizeof(uint32_t) * e->canon_total, cudaMemcpyDeviceToHost));
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_live_count(trs_gpu_engine* e, uint64_t* live) {
+    if (!e || !e->loaded || !live) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
+    cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    unsigned long long* d = reinterpret_cast<unsigned long long*>(e->d_blocksum + kMaxGrid);  // scratch words
+    CUDA_TRY(e, cudaMemsetAsync(d, 0, sizeof(*d), e->stream));
+    const uint32_t* A = e->d_arena[c.arena];
+    const int blocks = e->sm_count * 8;
+    switch (e->W) {
+        case 8: count_live<8><<<blocks, 256, 0, e->stream>>>(A, c.bump, d); break;
+        case 16: count_live<16><<<blocks, 256, 0, e->stream>>>(A, c.bump, d); break;
+        default: count_live<32><<<blocks, 256, 0, e->stream>>>(A, c.bump, d); break;
+    }
+    unsigned long long v = 0;
+    CUDA_TRY(e, cudaMemcpyAsync(&v, d, sizeof(v), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    *live = v;
+    return TRS_GPU_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <int ILP>
+void launch_probe(uint32_t vec, int grid, const uint32_t* data, uint64_t mask, const uint32_t* idx, uint32_t n,
+                  uint32_t* sink) {
+    switch (vec) {
+        case 1: gather_probe_kernel<1, ILP><<<grid, 512>>>(data, mask, idx, n, sink); break;
+        case 2: gather_probe_kernel<2, ILP><<<grid, 512>>>(data, mask, idx, n, sink); break;
+        case 4: gather_probe_kernel<4, ILP><<<grid, 512>>>(data, mask, idx, n, sink); break;
+        default: gather_probe_kernel<8, ILP><<<grid, 512>>>(data, mask, idx, n, sink); break;
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int trs_gpu_gather_probe_ex(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t ilp, uint32_t iters,
+                            double* gbps) {
     if (!gbps || (bytes_per_access != 4 && bytes_per_access != 8 && bytes_per_access != 16 && bytes_per_access != 32))
         return TRS_GPU_INVALID;
+    if (ilp != 1 && ilp != 2 && ilp != 4 && ilp != 8 && ilp != 16) return TRS_GPU_INVALID;
     if (cudaSetDevice(device) != cudaSuccess) return TRS_GPU_CUDA;
     uint64_t words = 1;
     while (words * 2 <= bytes / 4) words *= 2;  // power of two: addressing is a mask
@@ -1676,11 +2027,12 @@ int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, 
     const uint64_t mask = (words - 1) & ~(uint64_t)(vec - 1);
     auto launch = [&]() {
         const int grid = sms * 4;  // 4 x 512 threads = a full SM
-        switch (vec) {
-            case 1: gather_probe_kernel<1><<<grid, 512>>>(data, mask, idx, n, sink); break;
-            case 2: gather_probe_kernel<2><<<grid, 512>>>(data, mask, idx, n, sink); break;
-            case 4: gather_probe_kernel<4><<<grid, 512>>>(data, mask, idx, n, sink); break;
-            default: gather_probe_kernel<8><<<grid, 512>>>(data, mask, idx, n, sink); break;
+        switch (ilp) {
+            case 1: launch_probe<1>(vec, grid, data, mask, idx, n, sink); break;
+            case 2: launch_probe<2>(vec, grid, data, mask, idx, n, sink); break;
+            case 4: launch_probe<4>(vec, grid, data, mask, idx, n, sink); break;
+            case 8: launch_probe<8>(vec, grid, data, mask, idx, n, sink); break;
+            default: launch_probe<16>(vec, grid, data, mask, idx, n, sink); break;
         }
     };
     launch();  // warm-up
@@ -1701,6 +2053,10 @@ int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, 
     if (err != cudaSuccess) return TRS_GPU_CUDA;
     *gbps = (double)n * iters * bytes_per_access / (ms * 1e-3) / 1e9;
     return TRS_GPU_OK;
+}
+
+int trs_gpu_gather_probe(int device, uint64_t bytes, uint32_t bytes_per_access, uint32_t iters, double* gbps) {
+    return trs_gpu_gather_probe_ex(device, bytes, bytes_per_access, 4, iters, gbps);
 }
 
 }  // extern "C"

@@ -29,7 +29,7 @@ struct ExportArgs {
     uint32_t* queue[3];  // queue[0]: [bump] work items, zeroed by the host
     uint32_t* map;       // [bump]
     uint32_t* newrc;     // [bump]
-    uint32_t* counters;  // [3] tail, head, pending (zeroed by the host)
+    uint32_t* counters;  // [4] tail, head, pending, dangling (zeroed by the host)
     uint32_t* hss;       // output columns (staging)
     uint32_t* args;      // [ma * n]
     uint32_t* rcs;
@@ -115,18 +115,30 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         }
         while (x) {
             const uint32_t* R = A + (size_t)x * W;
+            if (h4.x == kDeadHead) {
+                // a live term references a collected slot: extract's
+                // DanglingReference (term_store.cpp:84-88)
+                atomicExch(X.counters + 3, x);
+                break;
+            }
             const uint32_t ar = arity[h4.x & kSymMask];
             // speculate that the walk continues into the first argument (S^k
             // numerals, list spines): its record load overlaps the reference
             // count round trip that decides it
             uint4 sh = make_uint4(0u, 0u, 0u, 0u), sa = sh;
-            if (ar) {
+            if (ar && a4.x != 0u && a4.x < bump) {
                 sh = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)a4.x * W));
                 sa = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)a4.x * W + kWArgs));
             }
             uint32_t next = 0;
             for (uint32_t j = 0; j < ar; ++j) {
                 const uint32_t c = j == 0 ? a4.x : j == 1 ? a4.y : j == 2 ? a4.z : j == 3 ? a4.w : __ldcg(R + kWArgs + j);
+                if (c == 0u || c >= bump) {
+                    // slot 0 or past the store: DanglingReference (term_store.cpp:84-88)
+                    atomicExch(X.counters + 3, 0xFFFFFFFFu);
+                    if (j == 0) a4.x = 0u;  // no speculated walk into it
+                    continue;
+                }
                 if (atomicAdd(X.newrc + c, 1u) == 0u) {
                     if (next == 0) {
                         next = c;  // keep walking: a chain stays in one thread
@@ -220,7 +232,7 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         const uint32_t ar = arity[sym];
         X.hss[k] = sym;
         X.rcs[k] = rc;
-        X.nf[k] = q0.y != 0;
+        X.nf[k] = epoch_nf(q0.y);
         for (uint32_t j = 0; j < X.ma; ++j)
             X.args[(size_t)j * n + k] = j < ar ? __ldcg(X.map + __ldcg(R + kWArgs + j)) : 0u;
         }

@@ -17,6 +17,7 @@ namespace trs_b200 {
 struct Frontier {
     uint32_t R;
     uint32_t M;
+    uint32_t flags;        // OR of the regions' kFlag* (the sweep that wrote them)
     const uint32_t* pref;  // [R + 1], pref[R] = M
     const uint32_t* off;   // [R]
 };
@@ -185,6 +186,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
     if (block_rank == 0 && threadIdx.x == 0) {
         region_off(P, cur ^ 1)[0] = 0;
         region_cnt(P, cur ^ 1)[0] = in.M;
+        P.region_flags[(cur ^ 1) * kMaxGrid] = 0u;
         P.ctl->nregions[cur ^ 1] = 1;
     }
     grid_sync(P.ctl, nblocks, epoch);

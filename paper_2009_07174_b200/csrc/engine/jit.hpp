@@ -155,7 +155,7 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
                                                                  : "fresh + " + std::to_string(I.subscriber) + "u";
                     std::snprintf(line, sizeof line,
                                   "            { uint32_t* F = rec<W>(arena, fresh + %uu);\n"
-                                  "              *reinterpret_cast<uint4*>(F) = make_uint4(%uu, 0u, %uu, %s);\n",
+                                  "              *reinterpret_cast<uint4*>(F) = make_uint4(%uu, tnext, %uu, %s);\n",
                                   k, I.symbol | ((uint32_t)I.cursor << kSymBits), (unsigned)I.indegree, sub.c_str());
                     body += line;
                     // the first argument quad always (zeros past the arity: sweep.cuh's build)
@@ -167,7 +167,7 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
                 } else {
                     std::snprintf(line, sizeof line,
                                   "            { uint32_t* R = rec<W>(arena, i);\n"
-                                  "              R[kWHead] = %uu;\n"
+                                  "              *reinterpret_cast<uint2*>(R) = make_uint2(%uu, tnext);\n"
                                   "              const uint32_t b[%d] = {",
                                   I.symbol | ((uint32_t)R.root_cursor << kSymBits), MAXA);
                     body += line;
@@ -202,7 +202,7 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
            "    switch (rule) {\n" +
            csrc + "        default: return 0u;\n    }\n}\n";
     src += "template <int W, bool S>\n__device__ __forceinline__ void gen_build(uint32_t rule, uint32_t* arena, uint32_t fresh,\n"
-           "    uint32_t i, uint32_t ar, const uint32_t (&gb)[TRS_GEN_MAXV]) {\n    switch (rule) {\n" +
+           "    uint32_t i, uint32_t ar, const uint32_t (&gb)[TRS_GEN_MAXV], uint32_t tnext) {\n    switch (rule) {\n" +
            build + "        default: break;\n    }\n}\n}  // namespace trs_b200\n#include \"sweep.cuh\"\n";
     return src;
 }

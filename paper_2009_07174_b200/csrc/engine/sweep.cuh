@@ -37,10 +37,11 @@ __device__ __forceinline__ uint32_t* bind_base(const Params& P, uint32_t* slist)
     return slist + 2 * kSmallCap + threadIdx.x;
 }
 
-enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild };
+enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild, kActDefer };
 
 struct Slab {
     uint32_t cur, end;  // warp-uniform: [cur, end) are this warp's unused fresh slots
+    uint32_t room;      // warp-uniform: the sweep's claims leave room for run-ahead
 };
 
 // Mark a warp's unused slab slots dead so collections and copies skip them.
@@ -49,6 +50,29 @@ __device__ __forceinline__ void abandon_slab(uint32_t* arena, Slab& slab) {
     const uint32_t lane = kSolo ? 0u : (threadIdx.x & 31);
     for (uint32_t x = slab.cur + lane; x < slab.end; x += kSolo ? 1u : 32u) rec<W>(arena, x)[kWHead] = kDeadHead;
     slab.cur = slab.end = 0;
+}
+
+// Width accounting (logical time): one rewrite in the histogram entry h.
+// Lanes whose entry equals the first rewriting lane's are folded into one
+// add (a whole wide sweep's warp usually shares one logical sweep).  A grid
+// sweep first adds into a CTA-shared window of kHistWin sweeps from its own
+// logical sweep (flushed once per CTA and sweep): every warp of a wide sweep
+// hitting the same global entry would serialise in one L2 slice.
+constexpr uint32_t kHistWin = 32;
+template <bool kSolo>
+__device__ __forceinline__ void hist_add(unsigned long long* h, bool on) {
+    if (kSolo) {
+        if (on) atomicAdd(h, 1ull);
+        return;
+    }
+    const uint32_t act = __ballot_sync(0xffffffffu, on);
+    if (!act) return;
+    const int first = __ffs(act) - 1;
+    const unsigned long long mine = reinterpret_cast<unsigned long long>(h);
+    const unsigned long long lead = __shfl_sync(0xffffffffu, mine, first);
+    const uint32_t same = __ballot_sync(0xffffffffu, on && mine == lead);
+    const int lane = threadIdx.x & 31;
+    if (on && (mine != lead || lane == first)) atomicAdd(h, mine != lead ? 1ull : (unsigned long long)__popc(same));
 }
 
 // Warp collectives of the warp step, or their one-lane identities when a
@@ -64,15 +88,32 @@ __device__ __forceinline__ uint32_t w_bcast(uint32_t v, int src) {
 }
 
 struct StepCtx {
-    uint32_t s;           // sweep number (nf epoch of this sweep)
+    uint32_t s;           // logical sweep of this physical sweep when there is no run-ahead (then they coincide)
     uint32_t bump;        // slot base of claims made during this sweep
     uint32_t* claim_ctr;  // slots claimed during this sweep (relative to bump)
     uint32_t* out;        // output region of the next frontier
     uint32_t* push_ctr;   // entries pushed into `out` (shared memory)
-    uint32_t* abort_flag; // shared flag raised with ctl->abort_capacity (may be null)
+    uint32_t* flags;      // CTA-shared kFlag* word of this sweep
     uint64_t cap;         // slots of the arena being swept (global or shared-memory resident)
     uint32_t slab;        // fresh slots a warp claims at a time (0: exactly what a step needs)
     uint32_t* bind;       // this thread's binding column (TRS_BIND)
+    // logical time (oracle_logical): slots derive at T = max(earliest sweep,
+    // argument nf epochs + 1); widths go to hist[T - t0]
+    uint32_t t0;          // the run's first logical sweep (earliest sweep of an input slot)
+    unsigned long long* hist;
+    uint32_t hist_cap;
+    unsigned long long* hwin;  // CTA-shared width window [hbase, hbase + kHistWin) (null: global adds)
+    uint32_t hbase;
+    uint32_t stamp;       // physical sweep mod 16, published with nf epochs
+    uint32_t ra;          // the run may run ahead: readiness by stamps, not by sweep number
+    // run-ahead: a lane carries on with a slot its own step made ready
+    // instead of pushing it to the next sweep; every step is backed by
+    // cont_cost reserved push entries of the output list (cont_room, null:
+    // no run-ahead), and slabs stop feeding it past claim_soft
+    int* cont_room;
+    uint32_t cont_cost;
+    uint32_t lone;        // single-CTA modes: push_ctr counts the whole next frontier
+    uint32_t claim_soft;
 };
 
 // Phase cycle accounting is compiled only into the profiling build
@@ -126,7 +167,8 @@ constexpr uint32_t kEntHasPayload = 1;
 template <int W, bool kRich, bool kSolo = false>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
                                               Slab& slab, bool valid, const uint32_t* entry, bool prof_req,
-                                              PhaseClock& pc) {
+                                              PhaseClock& pc, bool may_cont, uint32_t& cont, uint32_t& tmax,
+                                              uint32_t& just_nf, uint32_t& pushes) {
     const bool prof = kProfBuild && prof_req;
     constexpr int MAXA = rec_args(W);
     // arguments any symbol of the program has: the specialisation knows it,
@@ -145,6 +187,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     }
     uint32_t act = kActNone;
     uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
+    uint32_t T = 0;  // logical sweep of this derive
     uint32_t a[MAXA];
     // level-synchronous matcher state (DPlan): children's first argument
     // quads, grandchild slot heads, and the argument quads of two slots
@@ -154,6 +197,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     uint32_t ga[kPlanArgSlots * 4];
     uint32_t cs_head = 0, cs_b[4] = {0, 0, 0, 0};  // collapse source record taken from registers
     uint32_t own_waiter = 0;  // the record's waiter word as loaded (the nf publication's first guess)
+    uint32_t own_epoch = 0;   // the record's epoch word (earliest derive sweep while not nf)
 #if TRS_GEN
     bool gb_ready = false;       // set by the match-table path; the walks bind through shared memory
     uint32_t gb[TRS_GEN_MAXV];  // the chosen rule's bindings, in registers (constant indices only)
@@ -168,6 +212,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             const uint4 q0 = *reinterpret_cast<const uint4*>(entry);
             i = q0.x;
             headw = q0.y;
+            own_epoch = rec<W>(arena, i)[kWEpoch];
             have = q0.z == kEntHasPayload;
             if (have) {
 #pragma unroll
@@ -189,6 +234,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             const uint4 h4 = *reinterpret_cast<const uint4*>(R);
             const uint4 a4 = *reinterpret_cast<const uint4*>(R + kWArgs);
             headw = h4.x;
+            own_epoch = h4.y;
             own_waiter = h4.w;
             a[0] = a4.x;
             a[1] = a4.y;
@@ -245,18 +291,36 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             }
         }
         if (prof) pc.mark(1, cep[0] ^ cep[MAXA - 1] ^ ca[0]);
+        // Logical derive sweep (oracle_logical): one past the slot's build or
+        // last rewrite, and past every argument's nf epoch.  An argument that
+        // is not nf -- or whose nf is too fresh to read: published in this
+        // physical sweep (without run-ahead: in this sweep, nf_read,
+        // sweep_engine.cpp:80-81; with run-ahead: by another lane, whose
+        // record writes need not be visible yet) -- is pending, and the slot
+        // waits on the first such argument (:173-178).
+        T = (own_epoch & kTminBit) ? max(own_epoch & ~kTminBit, C.t0) : C.t0;
         bool pending = false;
 #pragma unroll
         for (int j = AE - 1; j >= 0; --j) {
-            // nf_read(c) at sweep s: nf since an earlier sweep (sweep_engine.cpp:80-81)
-            if ((uint32_t)j >= cursor && (uint32_t)j < ar && (cep[j] == 0 || cep[j] >= s)) {
-                pending = true;
-                wpos = j;
+            if ((uint32_t)j < ar) {
+                const uint32_t e = cep[j];
+                const bool ready = epoch_nf(e) && (C.ra ? (((e >> kEpochBits) & kStampMask) != C.stamp ||
+                                                          a[j] == just_nf)
+                                                       : (e & kEpochMask) < s);
+                if (ready) {
+                    T = max(T, (e & kEpochMask) + 1);
+                } else {
+                    pending = true;
+                    wpos = j;
+                }
             }
         }
         if (pending) {
             act = kActWait;
             wchild = pick(a, wpos);
+        } else if (T - C.t0 >= C.hist_cap || T >= kEpochMask - 1) {
+            // past the width histogram: the host grows it (kPlanTrace)
+            act = kActDefer;
         } else if (pl.fast) {
             planned = true;
             // level 2: grandchild slots (nf below an nf child: stable)
@@ -447,13 +511,15 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             uint32_t off = 0;
             if (lane == 0) off = atomicAdd(C.claim_ctr, size);
             off = w_bcast<kSolo>(off, 0);
+            // run-ahead feeds on the slots the sweep's worst case leaves over
+            slab.room = (uint64_t)off + size <= C.claim_soft ? 1u : 0u;
             const uint64_t start = (uint64_t)C.bump + off;
             if (start + total > C.cap) {
                 // not even this step's slots fit: the reference raises
                 // Capacity when get_new_index finds no slot (sweep_engine.cpp:221-226)
                 if (lane == 0) {
                     atomicExch(&P.ctl->abort_capacity, 1u);
-                    if (C.abort_flag) *C.abort_flag = 1u;
+                    atomicOr(C.flags, kFlagCapacity);
                 }
                 if (act == kActBuild) act = kActNone;
             } else {
@@ -473,7 +539,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 
     // ---- apply
     uint32_t npush = 0, push1 = 0, push_mask = 0;
-    bool rewrote = false;
+    bool rewrote = false, root_push = false;
     // Each lane makes at most one round trip to a waiter word: subscribe to
     // a pending child (Wait) or publish its own nf (Nf, Collapse).  Both are
     // issued as ONE compare-and-swap after the branches below, so a warp
@@ -487,7 +553,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         wval = i;
     } else if (act == kActNf) {
         uint32_t* R = rec<W>(arena, i);
-        R[kWEpoch] = s;
+        R[kWEpoch] = T | (C.stamp << kEpochBits);
+        tmax = max(tmax, T);
+        just_nf = i;
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -526,7 +594,9 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         for (int j = 0; j < MAXA; ++j)
             if ((uint32_t)j >= sar) b[j] = 0;
         uint32_t* R = rec<W>(arena, i);
-        *reinterpret_cast<uint2*>(R) = make_uint2(shead, s);
+        *reinterpret_cast<uint2*>(R) = make_uint2(shead, T | (C.stamp << kEpochBits));
+        tmax = max(tmax, T);
+        just_nf = i;
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
@@ -540,7 +610,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
 #if TRS_GEN
-        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb);
+        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb, kTminBit | (T + 1));
 #else
         const uint32_t nfresh = Rl.new_slots;
         for (uint32_t k = 0; k <= nfresh; ++k) {
@@ -561,7 +631,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             if (k < nfresh) {
                 uint32_t sub = I.subscriber == kNone ? 0u : I.subscriber == kRootSub ? i : fresh + I.subscriber;
                 uint32_t* F = rec<W>(arena, fresh + k);
-                *reinterpret_cast<uint4*>(F) = make_uint4(I.symbol | ((uint32_t)I.cursor << kSymBits), 0u, I.indegree, sub);
+                *reinterpret_cast<uint4*>(F) =
+                    make_uint4(I.symbol | ((uint32_t)I.cursor << kSymBits), kTminBit | (T + 1), I.indegree, sub);
                 // argument quads past the arity are never read, except the
                 // first: a planned match loads a child's first quad whole and
                 // follows a grandchild slot from it before the child's head is
@@ -575,7 +646,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                             make_uint4(b[q * 4], b[q * 4 + 1], b[q * 4 + 2], b[q * 4 + 3]);
             } else {
                 uint32_t* R = rec<W>(arena, i);
-                R[kWHead] = I.symbol | ((uint32_t)Rl.root_cursor << kSymBits);
+                *reinterpret_cast<uint2*>(R) =
+                    make_uint2(I.symbol | ((uint32_t)Rl.root_cursor << kSymBits), kTminBit | (T + 1));
                 store_args<W>(R, b, ar > iar ? ar : iar);
             }
             // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
@@ -587,9 +659,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         }
 #endif
         push_mask = Rl.push_mask;
-        npush = __popc(push_mask) + (Rl.root_wait == kNone ? 1u : 0u);
+        root_push = Rl.root_wait == kNone;
         push1 = i;
         rewrote = true;
+    } else if (act == kActDefer) {
+        atomicMax(&P.ctl->hist_need, T - C.t0 + 1);
+        atomicOr(C.flags, kFlagHist);
     }
     // the rewritten root drops its old children (after the additions, as
     // the reference orders them; sweep_engine.cpp:255-256)
@@ -600,6 +675,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             rc_upd<kSolo>(rec<W>(arena, a[j]) + kWRc, -1);
         }
     }
+    uint32_t wake = 0;  // the parent this lane's nf publication woke
     if (wword) {
         uint32_t old = atomicCAS(wword, wcmp, wval);
         if (act == kActWait) {
@@ -616,15 +692,58 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 wcmp = old;
                 old = atomicCAS(wword, wcmp, kWoken);
             }
-            if (old != 0 && old != kWoken) {
-                npush = 1;
-                push1 = old;
-            }
+            if (old != 0 && old != kWoken) wake = old;
         }
+    }
+    // ---- run-ahead: carry on with one slot this step made ready -- the woken
+    // parent, else the rewritten root when it can derive next, else the first
+    // ready fresh node -- at its logical sweep, instead of pushing it.  The
+    // slot's own writes are this lane's or older than this physical sweep,
+    // and its arguments' readiness is judged as above, so what it reads is
+    // what the reference would read.  Every continued step is backed by
+    // cont_cost reserved output entries (a refused reservation pushes).
+    bool want = may_cont && slab.room != 0u && (wake != 0u || (act == kActBuild && (push_mask != 0u || root_push)));
+    if (C.cont_room) {
+        const uint32_t wm = kSolo ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
+        if (wm) {
+            uint32_t ok = 0;
+            if (lane == 0) {
+                const int need = __popc(wm) * (int)C.cont_cost;
+                const int before = atomicSub(C.cont_room, need);
+                if (before >= need)
+                    ok = 1;
+                else
+                    atomicAdd(C.cont_room, need);
+            }
+            if (!w_bcast<kSolo>(ok, 0)) want = false;
+        }
+    } else {
+        want = false;
+    }
+    cont = 0;
+    if (want) {
+        if (wake) {
+            cont = wake;
+        } else if (root_push) {
+            cont = i;
+            root_push = false;
+        } else {
+            cont = fresh + (uint32_t)(__ffs(push_mask) - 1);
+            push_mask &= push_mask - 1;
+        }
+    } else if (wake) {
+        npush = 1;
+        push1 = wake;
+    }
+    if (act == kActBuild) npush = __popc(push_mask) + (root_push ? 1u : 0u);
+    if (act == kActDefer) {
+        npush = 1;
+        push1 = i;
     }
     long long c3 = prof ? clock64() : 0;
     if (prof) pc.t[2] += c3 - c2;
 
+    pushes += npush;
     // ---- next frontier: one shared-memory reservation per warp step
     const uint32_t pincl = w_scan<kSolo>(npush);
     const uint32_t ptotal = w_bcast<kSolo>(pincl, 31);
@@ -636,7 +755,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         if (npush) {
             if (act == kActBuild) {
                 const DRule& Rl = G.rules[rule];
-                uint32_t mask = push_mask | (Rl.root_wait == kNone ? (1u << Rl.new_slots) : 0u);
+                uint32_t mask = push_mask | (root_push ? (1u << Rl.new_slots) : 0u);
                 while (mask) {
                     const uint32_t k = __ffs(mask) - 1;
                     mask &= mask - 1;
@@ -687,8 +806,28 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         }
     }
     if (prof) pc.t[3] += clock64() - c3;
+    if (C.hwin) {
+        const bool win = rewrote && T - C.hbase < kHistWin;
+        hist_add<kSolo>(C.hwin + (T - C.hbase), win);
+        hist_add<kSolo>(C.hist + (T - C.t0), rewrote && !win);
+    } else {
+        hist_add<kSolo>(C.hist + (T - C.t0), rewrote);
+    }
     if (kSolo) return rewrote ? 1u : 0u;
     return __popc(__ballot_sync(0xffffffffu, rewrote));
+}
+
+// Run-ahead output entries per CTA per grid sweep, at most.
+constexpr uint32_t kMaxSlack = 1u << 20;
+
+// Whether a lane that has taken `steps` run-ahead steps for its current entry
+// may take another (the physical sweep must still end, where the step budget
+// and headroom are checked).
+__device__ __forceinline__ bool ra_more(const Params& P, const StepCtx& C, uint32_t steps) {
+    // a lone chain (single-CTA modes, nothing pushed for the next sweep yet)
+    // holds nothing back and runs on; otherwise the pushed work would wait
+    // for the chain's end, so a lane stops after P.ra_steps
+    return steps < P.ra_steps || (C.lone && steps < 4096u && *(volatile uint32_t*)C.push_ctr == 0u);
 }
 
 // All warps of CTAs [block_rank, nblocks) process the frontier in q-entry
@@ -698,25 +837,28 @@ template <int W, bool kRich>
 __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const Prog& G, uint32_t* arena,
                                                           const StepCtx& C, const Frontier& F,
                                                           const uint32_t* __restrict__ in, uint32_t block_rank,
-                                                          uint32_t nblocks, Slab& slab, bool prof, PhaseClock& pc) {
+                                                          uint32_t nblocks, Slab& slab, bool prof, PhaseClock& pc,
+                                                          uint32_t& tmax) {
     const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t gw = nblocks * kWarps;
     const uint32_t q = chunk_lanes(F.M, nblocks);
     unsigned long long rw = 0;
+    uint32_t cont = 0, just_nf = 0, pushes = 0;
     if (kRich) {
         for (uint32_t k = block_rank * kWarps + warp; k * q < F.M; k += gw) {
             const uint32_t v = k * q + lane;
             const bool valid = lane < q && v < F.M;
             const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * W : in;
-            rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc);
+            rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc,
+                                      false, cont, tmax, just_nf, pushes);
         }
         return lane == 0 ? rw : 0ull;
     }
-    // Dense entries, software-pipelined over a warp's chunks: the slot ids
-    // of the chunk after next are loaded, and the records of the next chunk
-    // prefetched into L2, while the current chunk derives -- a wide sweep
-    // hands each warp dozens of chunks, and their entry -> record chain would
-    // otherwise be paid in full, one chunk after another.
+    // Dense entries.  Each lane walks its own entries (k * q + lane, k += gw),
+    // software-pipelined: the slot ids of the entry after next are loaded,
+    // and the next entry's record prefetched into L2, while the current one
+    // derives (a wide sweep hands each warp dozens of chunks).  A lane whose
+    // step made a slot ready runs ahead with it before taking its next entry.
     auto slot_of = [&](uint32_t kk) -> uint32_t {
         const uint32_t v = kk * q + lane;
         return (lane < q && v < F.M) ? in[frontier_phys(F, v)] : 0u;  // generic: the list may be shared memory
@@ -724,16 +866,26 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     uint32_t k = block_rank * kWarps + warp;
     uint32_t s0 = k * q < F.M ? slot_of(k) : 0u;
     uint32_t s1 = (k + gw) * q < F.M ? slot_of(k + gw) : 0u;
-    for (; k * q < F.M; k += gw) {
-        const uint32_t s2 = (k + 2 * gw) * q < F.M ? slot_of(k + 2 * gw) : 0u;
-        // generic prefetch: a no-op when the arena is the shared-memory resident one
-        if (s1) asm volatile("prefetch.L2 [%0];" ::"l"(rec<W>(arena, s1)));
-        const uint32_t v = k * q + lane;
-        const bool valid = lane < q && v < F.M;
-        const uint32_t slot = s0;
-        rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, &slot, prof && (TRS_B200_PROFILE || warp == 0), pc);
-        s0 = s1;
-        s1 = s2;
+    uint32_t steps = 0;
+    for (;;) {
+        const bool own = lane < q && k * q + lane < F.M;
+        if (!__any_sync(0xffffffffu, cont != 0u || own)) break;
+        uint32_t slot = cont;
+        if (cont) {
+            ++steps;
+        } else if (own) {
+            const uint32_t s2 = (k + 2 * gw) * q < F.M ? slot_of(k + 2 * gw) : 0u;
+            // generic prefetch: a no-op when the arena is the shared-memory resident one
+            if (s1) asm volatile("prefetch.L2 [%0];" ::"l"(rec<W>(arena, s1)));
+            slot = s0;
+            s0 = s1;
+            s1 = s2;
+            k += gw;
+            steps = 0;
+            pushes = 0;
+        }
+        rw += warp_step<W, kRich>(P, G, arena, C, slab, slot != 0u, &slot, prof && (TRS_B200_PROFILE || warp == 0),
+                                  pc, ra_more(P, C, steps), cont, tmax, just_nf, pushes);
     }
     return lane == 0 ? rw : 0ull;
 }
@@ -741,15 +893,20 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
 // ---------------------------------------------------------------------------
 
 struct Local {
-    uint32_t sweep, cur, arena, bump;
+    uint32_t sweep, cur, arena, bump;  // sweep: physical sweeps of this run
     unsigned long long total, maxw;
     uint32_t gc_runs, small_sweeps, last_gc, peak_bump;
     unsigned long long gc_ns;
-    uint32_t sweep0;  // trace records index sweeps from here
+    uint32_t sweep0;  // logical sweeps before this run (input slots derive from sweep0 + 1)
+    // run-ahead state: `ra_narrow` consecutive sweeps of at most ra_kill
+    // entries switch it on (a latency-bound phase), a wider sweep off again;
+    // once it has run, argument readiness is judged by publication stamps
+    // (logical and physical sweeps no longer coincide)
+    uint32_t ra_narrow, ra_on, ra_used;
 };
 
 __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
-    L.sweep = __ldcg(&c->sweep);
+    L.sweep = __ldcg(&c->psweep);
     L.cur = __ldcg(&c->cur);
     L.arena = __ldcg(&c->arena);
     L.bump = __ldcg(&c->bump);
@@ -761,10 +918,13 @@ __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
     L.peak_bump = __ldcg(&c->peak_bump);
     L.gc_ns = __ldcg(&c->gc_ns);
     L.sweep0 = __ldcg(&c->sweep0);
+    L.ra_narrow = __ldcg(&c->ra_narrow);
+    L.ra_on = __ldcg(&c->ra_on);
+    L.ra_used = __ldcg(&c->ra_used);
 }
 
 __device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
-    c->sweep = L.sweep;
+    c->psweep = L.sweep;
     c->cur = L.cur;
     c->arena = L.arena;
     c->bump = L.bump;
@@ -775,6 +935,9 @@ __device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
     c->last_gc_sweep = L.last_gc;
     c->peak_bump = L.peak_bump;
     c->gc_ns = L.gc_ns;
+    c->ra_narrow = L.ra_narrow;
+    c->ra_on = L.ra_on;
+    c->ra_used = L.ra_used;
     __threadfence();
 }
 
@@ -784,7 +947,7 @@ enum Plan : uint32_t { kPlanSweep, kPlanGc, kPlanGrow, kPlanFinish, kPlanTrace }
 __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32_t m, bool just_collected,
                                          uint32_t nwarps) {
     const uint32_t s = L.sweep + 1;
-    if (s - L.sweep0 > P.trace_cap) return kPlanTrace;
+    if (s > P.trace_cap) return kPlanTrace;
     if (m == 0) return kPlanFinish;
     // worst case: every frontier slot rewrites with the largest template,
     // plus what slab hand-offs can strand (ensure_headroom, sweep_engine.cpp:290-303)
@@ -806,7 +969,9 @@ __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32
 
 __device__ __forceinline__ void record(const Params& P, uint32_t s, unsigned long long width, const Local& L,
                                        uint32_t m, uint32_t mode, uint64_t ns) {
-    const uint32_t k = s - L.sweep0;
+    // physical sweep record (diagnostics; the reference's widths are the
+    // logical histogram, Params::hist)
+    const uint32_t k = s;
     if (k == 0 || k > P.trace_cap) return;
     trs_gpu_sweep_record r;
     r.sweep = k;
@@ -829,6 +994,11 @@ __device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nbloc
                                    uint32_t* f_off, Smem& sm, unsigned long long* width) {
     const uint32_t t0 = threadIdx.x, t1 = threadIdx.x + kBlock;
     const uint32_t R = __ldcg(&P.ctl->nregions[buf]);
+    // the regions' flags, ORed over the CTA (every thread reads its regions)
+    uint32_t fl = t0 < R ? __ldcg(P.region_flags + buf * kMaxGrid + t0) : 0u;
+    if (t1 < R) fl |= __ldcg(P.region_flags + buf * kMaxGrid + t1);
+    const uint32_t flags = (__syncthreads_or((int)(fl & kFlagCapacity)) ? kFlagCapacity : 0u) |
+                           (__syncthreads_or((int)(fl & kFlagHist)) ? kFlagHist : 0u);
     if (nblocks <= kBlock) {
         // one region per thread: warp scans, then warp 0 scans the warp totals
         const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -870,6 +1040,7 @@ __device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nbloc
         Frontier F;
         F.R = R;
         F.M = M;
+        F.flags = flags;
         F.pref = f_pref;
         F.off = f_off;
         return F;
@@ -924,6 +1095,7 @@ __device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nbloc
     Frontier F;
     F.R = R;
     F.M = tot0 + tot1;
+    F.flags = flags;
     F.pref = f_pref;
     F.off = f_off;
     return F;
@@ -933,11 +1105,63 @@ __device__ Frontier stage_frontier(const Params& P, uint32_t buf, uint32_t nbloc
 struct SmallState {
     uint32_t count[2];  // frontier counts: [sc] being read, [sc ^ 1] being pushed
     uint32_t claim;     // slots claimed during the current sweep
-    uint32_t abort;     // a claim did not fit the fixed capacity
+    uint32_t flags;     // kFlag* raised in these sweeps
     uint32_t sc;
-    uint32_t pad[3];
+    int cont_room;      // output entries left for run-ahead steps this sweep
+    uint32_t pad[2];
     Local L;            // hand-over from warp mode to the whole CTA
 };
+
+// Run-ahead switches on after P.ra_warm consecutive sweeps of at most
+// P.ra_kill entries (a latency-bound phase: fib, Ackermann, reverse,
+// mergesort) and off at a wider one: lanes that ran ahead reach a wide phase
+// out of step, and a warp of lanes on different rules diverges.
+__device__ __forceinline__ void ra_track(const Params& P, Local& L, uint32_t m) {
+    if (!P.runahead) return;
+    if (m > P.ra_kill) {
+        L.ra_narrow = 0;
+        L.ra_on = 0;
+    } else if (++L.ra_narrow >= P.ra_warm) {
+        L.ra_on = 1;
+        L.ra_used = 1;
+    }
+}
+
+// The step context of physical sweep s over m frontier entries, swept by
+// nwarps warps.  Run-ahead gets the arena slots the sweep's worst case
+// (plan) leaves over, with a margin of two slabs (or two warp steps) per warp.
+__device__ __forceinline__ StepCtx make_ctx(const Params& P, const Local& L, uint32_t s, uint32_t* claim_ctr,
+                                            uint32_t* out, uint32_t* push_ctr, uint32_t* flags, uint64_t cap,
+                                            uint32_t slab, uint32_t* slist, uint32_t m, uint32_t nwarps,
+                                            int* cont_room) {
+    StepCtx C;
+    C.s = L.sweep0 + s;
+    C.bump = L.bump;
+    C.claim_ctr = claim_ctr;
+    C.out = out;
+    C.push_ctr = push_ctr;
+    C.flags = flags;
+    C.cap = cap;
+    C.slab = slab;
+    C.bind = bind_base(P, slist);
+    C.t0 = L.sweep0 + 1;
+    C.hist = P.hist;
+    C.hist_cap = P.hist_cap;
+    C.hwin = nullptr;
+    C.hbase = C.s;
+    C.stamp = s & kStampMask;
+    C.ra = L.ra_used;
+    // run-ahead pays in narrow sweeps of latency-bound phases (a lane's chain
+    // of dependent steps without a barrier between them); in a wide sweep the
+    // lanes of a warp stay on one rule path each only if they stay in step
+    C.cont_room = (L.ra_on && m <= P.ra_max) ? cont_room : nullptr;
+    C.cont_cost = P.max_new + 1;
+    C.lone = nwarps <= kWarps ? 1u : 0u;
+    const uint64_t worst = (uint64_t)m * P.max_new + 2ull * nwarps * max(slab, 32u * P.max_new) + 1;
+    const uint64_t room = cap > (uint64_t)L.bump + worst ? cap - L.bump - worst : 0ull;
+    C.claim_soft = room > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)room;
+    return C;
+}
 
 // Copy records [0, n) between arenas (global <-> shared memory), CTA-wide.
 template <int W>
@@ -1025,7 +1249,8 @@ __device__ uint32_t local_gc(const Params& P, const Prog& G, Smem& sm, uint32_t*
 // Warp 0 of CTA 0 runs sweeps alone while the frontier fits one warp.
 template <int W>
 __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, SmallState& ss, Local& L,
-                            bool& just_collected, Slab& slab, uint32_t* arena, uint64_t cap, uint32_t slab_size) {
+                            bool& just_collected, Slab& slab, uint32_t* arena, uint64_t cap, uint32_t slab_size,
+                            uint32_t& tmax) {
     const uint32_t lane = threadIdx.x & 31;
     PhaseClock pc;
     const bool prof = kProfBuild && P.profile == 1 && lane == 0;
@@ -1049,13 +1274,22 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                     if (plan(P, L, 1, just_collected, 1) != kPlanSweep) break;
                     just_collected = false;
                     const uint32_t s = L.sweep + 1;
+                    ra_track(P, L, 1);
                     const long long cs = prof ? clock64() : 0;
                     ss.count[sc1 ^ 1] = 0;
                     ss.claim = 0;
-                    StepCtx C{s, L.bump, &ss.claim, slist + (sc1 ^ 1) * kSmallCap, &ss.count[sc1 ^ 1], &ss.abort,
-                              cap, slab_size, bind_base(P, slist)};
-                    const uint32_t width =
-                        warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc1 * kSmallCap, prof, pc);
+                    ss.cont_room = (int)(kSmallCap - (P.max_new + 1));
+                    const StepCtx C = make_ctx(P, L, s, &ss.claim, slist + (sc1 ^ 1) * kSmallCap, &ss.count[sc1 ^ 1],
+                                               &ss.flags, cap, slab_size, slist, 1, 1, &ss.cont_room);
+                    uint32_t width = 0, cont = 0, steps = 0, just_nf = 0, pushes = 0;
+                    uint32_t slot = slist[sc1 * kSmallCap];
+                    for (;;) {
+                        width += warp_step<W, false, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                                                           ra_more(P, C, steps), cont, tmax, just_nf, pushes);
+                        if (!cont) break;
+                        slot = cont;
+                        ++steps;
+                    }
                     L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
                     L.peak_bump = max(L.peak_bump, L.bump);
                     L.total += width;
@@ -1073,7 +1307,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                         P.ctl->prof[6] += pc.steps;
                         pc = PhaseClock{};
                     }
-                    if (L.total > P.step_budget || ss.abort) break;
+                    if (L.total > P.step_budget || ss.flags) break;
                 }
                 ss.L = L;
             }
@@ -1083,8 +1317,9 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             t_prev = __shfl_sync(0xffffffffu, t_prev, 0);
             slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);
             slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
+            slab.room = __shfl_sync(0xffffffffu, slab.room, 0);
             __syncwarp();
-            if (L.total > P.step_budget || ss.abort) break;
+            if (L.total > P.step_budget || ss.flags) break;
             if (ss.count[ss.sc] == 1) break;  // stopped by plan or headroom: the caller decides
             continue;
         }
@@ -1093,25 +1328,45 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         if (plan(P, L, m, just_collected, 1) != kPlanSweep) break;
         just_collected = false;
         const uint32_t s = L.sweep + 1;
+        ra_track(P, L, m);
         const long long cs = prof ? clock64() : 0;
         if (lane == 0) {
             ss.count[sc ^ 1] = 0;
             ss.claim = 0;
+            ss.cont_room = (int)(kSmallCap - (P.max_new + 1) * m);
         }
         __syncwarp();
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
-                  bind_base(P, slist)};
-        uint32_t width;
+        const StepCtx C = make_ctx(P, L, s, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.flags,
+                                   cap, slab_size, slist, m, 1, &ss.cont_room);
+        uint32_t width = 0;
         if (TRS_GEN && W != 8 && m == 1) {
             // one entry, specialised wide-record kernel: lane 0 alone for this sweep
             uint32_t w1 = 0;
-            if (lane == 0) w1 = warp_step<W, false, true>(P, G, arena, C, slab, true, slist + sc * kSmallCap, prof, pc);
+            if (lane == 0) {
+                uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
+                uint32_t slot = slist[sc * kSmallCap];
+                for (;;) {
+                    w1 += warp_step<W, false, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                                                    ra_more(P, C, steps), cont, tmax, just_nf, pushes);
+                    if (!cont) break;
+                    slot = cont;
+                    ++steps;
+                }
+            }
             width = __shfl_sync(0xffffffffu, w1, 0);
             slab.cur = __shfl_sync(0xffffffffu, slab.cur, 0);  // the slab is warp-uniform state
             slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
+            slab.room = __shfl_sync(0xffffffffu, slab.room, 0);
         } else {
-            const bool valid = lane < m;
-            width = warp_step<W, false>(P, G, arena, C, slab, valid, slist + sc * kSmallCap + lane, prof, pc);
+            uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
+            uint32_t slot = lane < m ? slist[sc * kSmallCap + lane] : 0u;
+            for (;;) {
+                width += warp_step<W, false>(P, G, arena, C, slab, slot != 0u, &slot, prof, pc,
+                                             ra_more(P, C, steps), cont, tmax, just_nf, pushes);
+                if (!__any_sync(0xffffffffu, cont != 0u)) break;
+                slot = cont;
+                ++steps;
+            }
         }
         __syncwarp();
         L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
@@ -1134,7 +1389,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         }
         t_prev = now;
         __syncwarp();
-        if (L.total > P.step_budget || ss.abort) break;
+        if (L.total > P.step_budget || ss.flags) break;
     }
 }
 
@@ -1151,7 +1406,7 @@ __device__ __forceinline__ void zero_next_claims(const Params& P, uint32_t sweep
 // CTA 0 runs sweeps out of shared memory while the frontier is small.
 template <int W>
 __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bool& just_collected,
-                          uint32_t* slist, SmallState& ss, const Frontier& F, Slab& slab) {
+                          uint32_t* slist, SmallState& ss, const Frontier& F, Slab& slab, uint32_t& tmax) {
     Ctl* ctl = P.ctl;
     const uint32_t cap_m = kSmallCap / (P.max_new + 1);
     const uint32_t exit_m = min(P.small_exit, cap_m);
@@ -1169,7 +1424,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     if (threadIdx.x == 0) {
         ss.count[0] = F.M;
         ss.sc = 0;
-        ss.abort = 0;
+        ss.flags = 0;
     }
     __syncthreads();
     uint32_t* arena = P.arena[L.arena];
@@ -1219,13 +1474,13 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         if (plan(P, L, m, just_collected, kWarps) != kPlanSweep) break;
         if (P.warp_mode && m <= 32) {
             if (warp == 0) {
-                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size);
+                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size, tmax);
                 if ((threadIdx.x & 31) == 0) ss.L = L;
             }
             __syncthreads();
             L = ss.L;
             just_collected = false;
-            if (L.total > P.step_budget || ss.abort) break;
+            if (L.total > P.step_budget || ss.flags) break;
             const uint32_t m2 = ss.count[ss.sc];
             if (m2 <= 32 && !(resident && m2 && (uint64_t)L.bump + (uint64_t)m2 * P.max_new + 1 > cap))
                 break;  // warp mode stopped for another reason (plan / empty)
@@ -1233,6 +1488,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         }
         just_collected = false;
         const uint32_t s = L.sweep + 1;
+        ra_track(P, L, m);
         const uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
         const bool profc = kProfBuild && P.profile == 1 && threadIdx.x == 0;
         const long long cs = profc ? clock64() : 0;
@@ -1240,16 +1496,17 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         if (threadIdx.x == 0) {
             ss.count[sc ^ 1] = 0;
             ss.claim = 0;
+            ss.cont_room = (int)(kSmallCap - (P.max_new + 1) * m);
         }
         __syncthreads();
-        Frontier Fs{1, m, nullptr, nullptr};
+        Frontier Fs{1, m, 0u, nullptr, nullptr};
         uint32_t zero_off = 0;
         Fs.off = &zero_off;
-        StepCtx C{s, L.bump, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.abort, cap, slab_size,
-                  bind_base(P, slist)};
+        const StepCtx C = make_ctx(P, L, s, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.flags, cap,
+                                   slab_size, slist, m, kWarps, &ss.cont_room);
         PhaseClock pc;
         unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
-                                                      profc, pc);
+                                                      profc, pc, tmax);
         const unsigned long long width = block_sum64(rw, sm);
         L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
         L.peak_bump = max(L.peak_bump, L.bump);
@@ -1269,7 +1526,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
             }
         }
         __syncthreads();
-        if (L.total > P.step_budget || ss.abort) break;
+        if (L.total > P.step_budget || ss.flags) break;
     }
     if (resident) leave_resident();
     // hand the frontier back to the grid as one region of the global list
@@ -1285,6 +1542,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     if (threadIdx.x == 0) {
         region_off(P, L.cur)[0] = 0;
         region_cnt(P, L.cur)[0] = m;
+        P.region_flags[L.cur * kMaxGrid] = ss.flags;
         ctl->nregions[L.cur] = 1;
         zero_next_claims(P, L.sweep);
         store_local(L, ctl);
@@ -1299,6 +1557,9 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     __shared__ uint32_t f_pref[kMaxGrid + 1];
     __shared__ uint32_t f_off[kMaxGrid];
     __shared__ uint32_t s_push;
+    __shared__ uint32_t s_flags;
+    __shared__ int s_cont;
+    __shared__ unsigned long long s_hwin[kHistWin];
     // stage the program tables; the single-CTA frontier lists follow them
     for (uint32_t o = threadIdx.x * 16; o < P.prog_bytes; o += kBlock * 16)
         *reinterpret_cast<uint4*>(smem_raw + o) = *reinterpret_cast<const uint4*>(P.prog + o);
@@ -1315,7 +1576,8 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     bool just_collected = false;
     uint32_t exit_status = kRunning;
     uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
-    Slab slab{0, 0};
+    Slab slab{0, 0, 1u};
+    uint32_t tmax = 0;  // latest nf epoch this thread published (the run's logical sweep count)
     Frontier F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
 
     bool gc_truncated = false;
@@ -1393,13 +1655,17 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             // ---- single-CTA mode: CTA 0 runs sweeps out of shared memory,
             // the rest of the grid parks in the barrier
             const uint32_t before = L.sweep;
-            if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss, F, slab);
+            if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss, F, slab, tmax);
             grid_sync(ctl, nblocks, epoch, /*park=*/blockIdx.x != 0);
             load_local(L, ctl);
             F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
-            if (__ldcg(&ctl->abort_capacity)) {
+            if (F.flags & kFlagCapacity) {
                 exit_status = kCapacity;
+                break;
+            }
+            if (F.flags & kFlagHist) {
+                exit_status = kNeedTrace;
                 break;
             }
             if (L.total > P.step_budget) {
@@ -1416,13 +1682,27 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         const uint64_t t0 = leader ? global_ns() : 0;
         const bool profsw = kProfBuild && P.profile && (P.profile == 1 || m <= P.profile);
         const long long cs = (profsw && leader) ? clock64() : 0;
-        if (threadIdx.x == 0) s_push = 0;
+        // output regions: CTA b's own entries need (max_new + 1) * count, and
+        // every CTA gets the same slack of the list buffer for run-ahead steps
+        const uint64_t base_ext = (uint64_t)(P.max_new + 1) * m;
+        const uint32_t slack = (P.runahead && !P.rich && P.list_cap > base_ext)
+                                   ? (uint32_t)min((P.list_cap - base_ext) / nblocks, (uint64_t)kMaxSlack)
+                                   : 0u;
+        ra_track(P, L, m);  // every CTA sees the same m
+        if (threadIdx.x == 0) {
+            s_push = 0;
+            s_flags = 0;
+            s_cont = (int)slack;
+        }
+        if (threadIdx.x < kHistWin) s_hwin[threadIdx.x] = 0ull;
         __syncthreads();
-        const uint32_t out_off = (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks, chunk_lanes(m, nblocks));
+        const uint32_t out_off =
+            (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks, chunk_lanes(m, nblocks)) + blockIdx.x * slack;
         uint32_t* claim_ctr = &P.blocksum[kMaxGrid + (s & 3)];
         if (leader) P.blocksum[kMaxGrid + ((s + 2) & 3)] = 0;
-        StepCtx C{s, L.bump, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push, nullptr,
-                  P.capacity, P.slab, bind_base(P, slist)};
+        StepCtx C = make_ctx(P, L, s, claim_ctr, P.list[L.cur ^ 1] + (size_t)out_off * (P.rich ? W : 1), &s_push,
+                             &s_flags, P.capacity, P.slab, slist, m, nwarps, &s_cont);
+        C.hwin = s_hwin;
         PhaseClock pc;
 #if TRS_B200_PROFILE
         // profiling build: the slowest warp's entry time of this sweep
@@ -1442,11 +1722,11 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         unsigned long long rw =
 #if TRS_B200_RICH_ENTRIES
             P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                          wprof, wpc)
+                                          wprof, wpc, tmax)
                    :
 #endif
                      cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
-                                           wprof, wpc);
+                                           wprof, wpc, tmax);
 #if TRS_B200_PROFILE
         if ((threadIdx.x & 31) == 0) atomicMax(&ctl->gcprof[s & 1], (unsigned long long)(clock64() - wt0));
         if (wprof) {
@@ -1455,11 +1735,14 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         }
         if (leader) pc = wpc;
 #endif
-        rw = block_sum64(rw, sm);
+        rw = block_sum64(rw, sm);  // ends synchronised: the width window is complete
+        if (threadIdx.x < kHistWin && s_hwin[threadIdx.x])
+            atomicAdd(P.hist + (C.hbase - C.t0 + threadIdx.x), s_hwin[threadIdx.x]);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
             region_cnt(P, L.cur ^ 1)[blockIdx.x] = s_push;
             P.region_rew[(L.cur ^ 1) * kMaxGrid + blockIdx.x] = rw;
+            P.region_flags[(L.cur ^ 1) * kMaxGrid + blockIdx.x] = s_flags;
         }
         if (leader) ctl->nregions[L.cur ^ 1] = nblocks;
         grid_sync(ctl, nblocks, epoch);
@@ -1475,7 +1758,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         if (leader) {
             record(P, s, width, L, m, 0, global_ns() - t0);
 #if TRS_B200_PROFILE
-            if (s - L.sweep0 <= P.trace_cap && s > L.sweep0) P.trace[s - L.sweep0 - 1].free_len = (uint32_t)__ldcg(&ctl->gcprof[s & 1]);
+            if (s <= P.trace_cap) P.trace[s - 1].free_len = (uint32_t)__ldcg(&ctl->gcprof[s & 1]);
             if (profsw)
                 for (int k = 0; k < 8; ++k) ctl->wmax_sum[k] += __ldcg(&ctl->wmax[s & 1][k]);
 #endif
@@ -1487,8 +1770,12 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
                 for (int k = 0; k < 4; ++k) ctl->prof[8 + k] += pc.sub[k];
             }
         }
-        if (__ldcg(&ctl->abort_capacity)) {
+        if (F.flags & kFlagCapacity) {
             exit_status = kCapacity;
+            break;
+        }
+        if (F.flags & kFlagHist) {
+            exit_status = kNeedTrace;
             break;
         }
         if (L.total > P.step_budget) {
@@ -1499,6 +1786,10 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     // leave no half-used slab behind: the host may copy or the next launch
     // may collect [0, bump)
     abandon_slab<W>(P.arena[L.arena], slab);
+    // the latest nf epoch of this launch; finish_run turns it into the
+    // logical sweep count
+    const uint32_t wt = __reduce_max_sync(0xffffffffu, tmax);
+    if ((threadIdx.x & 31) == 0 && wt) atomicMax(&ctl->tmax, wt);
     if (leader) {
         store_local(L, ctl);
         ctl->status = exit_status;

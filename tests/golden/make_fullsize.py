@@ -10,7 +10,8 @@ it records
   * from the reference seq engine (`normalize`, seq_engine.cpp:136-192):
     total rewrites and the SHA-1 of the canonical DAG words of the normal
     form (pre-order, first-visit ids, (symbol, child ids)
-    per node), their length and node count;
+    per node), their length and node count, and the position-keyed hash
+    trs_gpu_canonical_all reports per root (api.canonical_hash);
   * from the reference sweep engine (`run`, sweep_engine.cpp:69-149): the
     per-sweep width vector's SHA-1, sweep count and max width, with its
     rewrite total and normal form asserted equal to the seq engine's
@@ -32,15 +33,18 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import ref  # noqa: E402
+from paper_2009_07174_b200 import api  # noqa: E402  (canonical_hash: a pure numpy function)
 from paper_2009_07174_b200 import workloads as W  # noqa: E402
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "fullsize_ref.json")
 
 
-def configs():
+def configs(max_seed: int = 8):
+    """BASELINE configs; shards s1..s8 of config 5, and up to max_seed for
+    the weak-scaling bench (rank r of N runs seeds 8r+1..8r+8)."""
     c = {k: v[0] for k, v in W.CONFIGS.items()}
-    c.update({f"fibbatch_s{s}": (lambda s=s: W.fib_batch(s)) for s in range(1, 9)})
-    c.update({f"sortbatch_s{s}": (lambda s=s: W.treemergesort_batch(s)) for s in range(1, 9)})
+    c.update({f"fibbatch_s{s}": (lambda s=s: W.fib_batch(s)) for s in range(1, max_seed + 1)})
+    c.update({f"sortbatch_s{s}": (lambda s=s: W.treemergesort_batch(s)) for s in range(1, max_seed + 1)})
     return c
 
 
@@ -54,6 +58,7 @@ def record(name: str, text: str, workers: int, sweep: bool) -> dict:
     assert sq.status == 0, sq.message
     words = sq.words.astype("<u4")
     row = {"rewrites": int(sq.rewrites), "words_sha1": sha1(words), "n_words": int(words.size),
+           "words_hash": str(api.canonical_hash(words)),
            "nodes": int(sq.n_nodes), "seq_seconds": round(sq.micros * 1e-6, 4),
            "generator": "oracle/_ref seq normalize"}
     print(f"{name}: seq {sq.rewrites} rewrites, {sq.n_nodes} nodes, {time.time() - t:.1f}s", flush=True)
@@ -91,9 +96,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workers", type=int, default=1)
     ap.add_argument("--no-sweep", action="store_true", help="seq words only")
+    ap.add_argument("--max-seed", type=int, default=8, help="config 5 shards up to this seed")
     ap.add_argument("names", nargs="*")
     a = ap.parse_args()
-    for name, fn in configs().items():
+    for name, fn in configs(a.max_seed).items():
         if a.names and name not in a.names:
             continue
         merge(name, record(name, fn(), a.workers, not a.no_sweep))

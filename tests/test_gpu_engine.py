@@ -119,7 +119,8 @@ def _pad_add(a, b):
 @pytest.mark.parametrize("opts", [dict(variant=2), dict(max_blocks=1), dict(small_enter=1 << 20, small_exit=1 << 20),
                                   dict(disable_small=1, gc_interval=3), dict(blocks_per_sm=1, small_enter=4),
                                   dict(profile=1), dict(disable_warp_mode=1, max_blocks=3), dict(disable_gc=1),
-                                  dict(small_enter=40, small_exit=40), dict(validate=1, gc_interval=1)])
+                                  dict(small_enter=40, small_exit=40), dict(validate=1, gc_interval=1),
+                                  dict(no_runahead=1), dict(no_runahead=1, disable_small=1)])
 @pytest.mark.parametrize("name", ["treemergesort_4_5_s7", "fibbatch64_s3", "unit_two_waiters", "transform6"])
 def test_knobs_do_not_change_results(engine, name, opts):
     g = CASES[name]
@@ -201,16 +202,16 @@ def test_resident_mode_is_invisible(engine, name, gc_interval):
     compactions) gives the same widths, rewrites and normal form as sweeping
     the store in HBM."""
     g = CASES[name]
-    outs = []
+    modes = []
     for no_resident in (0, 1):
         o = api.make_options(gc_interval=gc_interval)
         o.reserved[1] = no_resident
         res = api.normalize_texts(g["text"], engine=engine, options=o)
-        outs.append(res)
+        modes.append(int(engine.phys_trace()["mode"].max()))  # physical sweeps: which mode ran them
         assert res.total_rewrites == g["rewrites"]
         np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
         np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
-    assert outs[0].trace["mode"].max() >= 1
+    assert modes[0] >= 1
 
 
 @pytest.mark.parametrize("k", [3, 6, 10, 20])
@@ -253,8 +254,16 @@ def test_trace_records(engine):
     res = run(engine, CASES["mergesort10_s3"]["text"])
     tr = res.trace
     assert list(tr["sweep"]) == list(range(1, len(tr) + 1))
-    assert (tr["n"] >= 2).all() and (tr["live_terms"] >= 1).all()
-    assert tr["rewrites"].max() <= res.total_rewrites
+    assert len(tr) == res.sweeps and tr["rewrites"].sum() == res.total_rewrites
+    assert tr["rewrites"][-1] == 0  # the empty sweep that ends the run (sweep_engine.cpp:147)
+    # physical step-loop iterations: no more than the logical sweeps, and
+    # together they executed every rewrite
+    ph = engine.phys_trace()
+    assert 1 <= len(ph) <= len(tr)
+    assert list(ph["sweep"]) == list(range(1, len(ph) + 1))
+    assert (ph["n"] >= 2).all() and (ph["live_terms"] >= 1).all()
+    assert ph["rewrites"].sum() == res.total_rewrites
+    assert engine.live_count() >= 1
 
 
 def _sha(widths):
@@ -409,7 +418,7 @@ def test_slab_size_does_not_change_results(engine, name, slab):
     np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
 
 
-@pytest.mark.parametrize("mode", ["default", "grid_only", "no_warp", "gc1", "interp"])
+@pytest.mark.parametrize("mode", ["default", "grid_only", "no_warp", "gc1", "interp", "no_runahead"])
 @pytest.mark.parametrize("seed", range(40))
 def test_random_programs_against_oracle(engine, seed, mode):
     """Random terminating systems (workloads.random_program; the oracle
@@ -420,7 +429,7 @@ def test_random_programs_against_oracle(engine, seed, mode):
     text = W.random_program(seed)
     o = port.run_text(text)
     opts = {"default": {}, "grid_only": {"disable_small": 1}, "no_warp": {"disable_warp_mode": 1},
-            "gc1": {"gc_interval": 1, "validate": 1}, "interp": {}}[mode]
+            "gc1": {"gc_interval": 1, "validate": 1}, "interp": {}, "no_runahead": {"no_runahead": 1}}[mode]
     opt = api.make_options(**opts)
     if mode == "interp":
         opt.reserved[1] = 2

@@ -169,3 +169,27 @@ def test_logical_matches_sweep_restatement_on_batches():
 def test_logical_step_budget():
     text = "sort T = A() | F(T);\nvar X : T;\neqn F(X) = F(F(X));\ninput F(A());\n"
     assert O.run_logical(text, step_budget=500).status == 1
+
+
+FULLSIZE = os.path.join(os.path.dirname(__file__), "golden", "fullsize_ref.json")
+
+
+@pytest.mark.skipif(not os.path.exists(FULLSIZE), reason="full-size fixture not generated")
+@pytest.mark.parametrize("name", ["fib18", "reverse16k", "ackermann36", "mergesort16k", "fibbatch_s1", "sortbatch_s3"])
+def test_logical_restatement_matches_fullsize_reference(name):
+    """At BASELINE size the logical-time restatement reproduces the
+    reference's own full-size results (tests/golden/make_fullsize.py):
+    rewrites, sweeps, width-vector and normal-form hashes."""
+    import hashlib
+
+    fx = json.load(open(FULLSIZE)).get(name)
+    if fx is None:
+        pytest.skip(f"{name} not in the fixture yet")
+    texts = {**{k: v[0] for k, v in W.CONFIGS.items()},
+             "fibbatch_s1": lambda: W.fib_batch(1), "sortbatch_s3": lambda: W.treemergesort_batch(3)}
+    o = O.run_logical(texts[name]())
+    assert o.status == 0 and o.rewrites == fx["rewrites"]
+    assert hashlib.sha1(o.words[0].astype("<u4").tobytes()).hexdigest() == fx["words_sha1"]
+    if "widths_sha1" in fx:
+        assert o.sweeps == fx["sweeps"]
+        assert hashlib.sha1(o.widths.astype("<u8").tobytes()).hexdigest() == fx["widths_sha1"]

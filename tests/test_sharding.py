@@ -22,7 +22,7 @@ def _free_port() -> int:
     return port
 
 
-def _worker(rank, world, port, shards, roots, out):
+def _worker(rank, world, port, roots, out):
     sys.path.insert(0, ROOT)
     import torch
 
@@ -32,7 +32,7 @@ def _worker(rank, world, port, shards, roots, out):
 
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    seeds = bench.my_shards(rank, world, shards)
+    seeds = bench.my_seeds(rank, world, "strong")
     texts = [W.fib_batch(s, roots=roots) for s in seeds]
     res = O.run_text(texts, words=True)  # one multi-root store per rank, like the engine
     rw = torch.tensor([float(res.rewrites)])
@@ -54,13 +54,13 @@ def test_sharded_batch_matches_single_process(world):
     from oracle import oracle as O
     from paper_2009_07174_b200 import workloads as W
 
-    shards, roots = 4, 8
-    covered = sorted(s for r in range(world) for s in bench.my_shards(r, world, shards))
+    shards, roots = 8, 4
+    covered = sorted(s for r in range(world) for s in bench.my_seeds(r, world, "strong"))
     assert covered == list(range(1, shards + 1))
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, shards, roots, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, roots, q)) for r in range(world)]
     for p in procs:
         p.start()
     got = q.get(timeout=120)
@@ -78,10 +78,23 @@ def test_sharded_batch_matches_single_process(world):
     assert max(p["sweeps"] for p in got["parts"]) == whole.sweeps
 
 
-def test_partition_uneven():
+def test_partition_strong_uneven():
+    """--scaling strong: one 8-shard batch split over the ranks."""
     sys.path.insert(0, ROOT)
     import bench
 
     for world in (1, 2, 3, 4, 8):
-        seen = [s for r in range(world) for s in bench.my_shards(r, world)]
+        seen = [s for r in range(world) for s in bench.my_seeds(r, world, "strong")]
         assert sorted(seen) == list(range(1, 9))
+
+
+def test_partition_weak():
+    """--scaling weak (the default): 8 shards of its own per rank, disjoint,
+    seeds 8r+1..8r+8, so N ranks cover seeds 1..8N."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    for world in (1, 2, 4, 8):
+        per = [bench.my_seeds(r, world, "weak") for r in range(world)]
+        assert all(len(p) == 8 for p in per)
+        assert sorted(s for p in per for s in p) == list(range(1, 8 * world + 1))

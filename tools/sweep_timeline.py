@@ -39,7 +39,7 @@ def main():
     for _ in range(2):
         eng.load(store)
         st = eng.run(opts)
-    tr = eng.trace()
+    tr = eng.phys_trace()  # physical step-loop iterations
     if args.save:
         np.save(args.save, tr)
     act = tr["active"].astype(np.int64)
