@@ -1,12 +1,15 @@
-// .trs front end: lexer, parser, resolver (counterpart of proj/src/parser.cpp).
-//
-// Same language and diagnostics as the reference (sections `sort`, `var`,
-// `eqn`, `input`/`Input`; optional `struct`; `%` line comments; constants
-// written `Name()`, bare names are variables), but every stage is
-// iterative: raw terms are flat post-order node arrays and resolution walks
-// them with an explicit stack in the reference's pre-order, so the
-// reference's resolver recursion (parser.cpp:443-491, which overflows an
-// 8 MiB stack near 16k nesting) has no counterpart here.
+// .trs front end: scanner, statement parser, resolver -- the language of
+// proj/src/parser.cpp (sections `sort`, `var`, `eqn`, `input`/`Input`;
+// optional `struct`; `%` line comments; constants written `Name()`, bare
+// names are variables) with the same located diagnostics, word for word
+// (tests/test_host.py checks them against the reference, including 600
+// mutated systems).  The design is this file's own: the text is scanned in
+// one pass into a token array through a character-class table, sections are
+// driven by a table of statement parsers over token indices, raw terms are
+// flat post-order node arrays, and resolution walks them with an explicit
+// stack in the reference's pre-order -- nothing recurses, so the reference
+// resolver's stack overflow near 16k nesting (parser.cpp:443-491, SURVEY.md
+// §8c) has no counterpart here.
 #include <cctype>
 
 #include "trs_host.hpp"
@@ -33,7 +36,13 @@ std::string format_error(std::string_view file, const ParseError& e) {
 
 namespace {
 
-enum class Tok { Ident, LParen, RParen, Comma, Semi, Equals, Pipe, Colon, End };
+// ---- scanner ---------------------------------------------------------------
+// The whole text is scanned up front into a token array (the parser then
+// works on index ranges of it).  Characters are classified by one table;
+// anything that is neither blank, `%` comment, punctuation nor a letter is
+// a lex error that is reported and skipped.
+
+enum class Tok : std::uint8_t { Ident, LParen, RParen, Comma, Semi, Equals, Pipe, Colon, End };
 
 struct Token {
     Tok kind = Tok::End;
@@ -41,84 +50,93 @@ struct Token {
     SourceSpan span;
 };
 
-bool reserved(std::string_view w) {
-    return w == "sort" || w == "var" || w == "eqn" || w == "input" || w == "Input" || w == "struct";
+enum CharClass : std::uint8_t { kBad, kBlank, kNewline, kComment, kAlpha, kDigit, kUnder, kPunct };
+
+struct CharTable {
+    CharClass cls[256];
+    Tok punct[256];
+    CharTable() {
+        for (int c = 0; c < 256; ++c) {
+            cls[c] = kBad;
+            punct[c] = Tok::End;
+            if (std::isalpha(c)) cls[c] = kAlpha;
+            if (std::isdigit(c)) cls[c] = kDigit;
+        }
+        cls[(unsigned char)' '] = cls[(unsigned char)'\t'] = cls[(unsigned char)'\r'] = kBlank;
+        cls[(unsigned char)'\n'] = kNewline;
+        cls[(unsigned char)'%'] = kComment;
+        cls[(unsigned char)'_'] = kUnder;
+        const std::pair<char, Tok> p[] = {{'(', Tok::LParen}, {')', Tok::RParen}, {',', Tok::Comma}, {';', Tok::Semi},
+                                          {'=', Tok::Equals}, {'|', Tok::Pipe},   {':', Tok::Colon}};
+        for (auto [c, t] : p) {
+            cls[(unsigned char)c] = kPunct;
+            punct[(unsigned char)c] = t;
+        }
+    }
+};
+
+const CharTable& char_table() {
+    static const CharTable t;
+    return t;
 }
 
-class Lexer {
-public:
-    Lexer(std::string_view src, std::vector<ParseError>& errors) : src_(src), errors_(errors) { next(); }
-    const Token& peek() const { return tok_; }
-    Token take() {
-        Token t = tok_;
-        next();
-        return t;
-    }
+// Section keywords (and `struct`) are not names.
+bool reserved(std::string_view w) {
+    static const std::string_view kw[] = {"sort", "var", "eqn", "input", "Input", "struct"};
+    for (std::string_view k : kw)
+        if (w == k) return true;
+    return false;
+}
 
-private:
-    void bump() {
-        if (src_[pos_] == '\n') {
-            ++line_;
-            col_ = 1;
-        } else {
-            ++col_;
+std::vector<Token> scan(std::string_view src, std::vector<ParseError>& errors) {
+    const CharTable& T = char_table();
+    std::vector<Token> out;
+    std::uint32_t line = 1, col = 1;
+    std::size_t i = 0;
+    auto advance = [&](std::size_t n) {
+        for (std::size_t k = 0; k < n; ++k, ++i) {
+            if (src[i] == '\n') {
+                ++line;
+                col = 1;
+            } else {
+                ++col;
+            }
         }
-        ++pos_;
-    }
-    void next() {
-        for (;;) {
-            for (;;) {
-                while (pos_ < src_.size() && (src_[pos_] == ' ' || src_[pos_] == '\t' || src_[pos_] == '\r' || src_[pos_] == '\n'))
-                    bump();
-                if (pos_ < src_.size() && src_[pos_] == '%') {
-                    while (pos_ < src_.size() && src_[pos_] != '\n') bump();
-                    continue;
-                }
+    };
+    while (i < src.size()) {
+        const unsigned char c = static_cast<unsigned char>(src[i]);
+        switch (T.cls[c]) {
+            case kBlank:
+            case kNewline: advance(1); break;
+            case kComment: {
+                std::size_t e = src.find('\n', i);
+                advance((e == std::string_view::npos ? src.size() : e) - i);
                 break;
             }
-            tok_.span = {line_, col_, 1};
-            if (pos_ >= src_.size()) {
-                tok_.kind = Tok::End;
-                tok_.text = {};
-                return;
+            case kPunct:
+                out.push_back({T.punct[c], src.substr(i, 1), {line, col, 1}});
+                advance(1);
+                break;
+            case kAlpha: {
+                std::size_t e = i + 1;
+                while (e < src.size()) {
+                    const CharClass k = T.cls[static_cast<unsigned char>(src[e])];
+                    if (k != kAlpha && k != kDigit && k != kUnder) break;
+                    ++e;
+                }
+                out.push_back({Tok::Ident, src.substr(i, e - i), {line, col, static_cast<std::uint32_t>(e - i)}});
+                advance(e - i);
+                break;
             }
-            const char c = src_[pos_];
-            Tok k;
-            switch (c) {
-                case '(': k = Tok::LParen; break;
-                case ')': k = Tok::RParen; break;
-                case ',': k = Tok::Comma; break;
-                case ';': k = Tok::Semi; break;
-                case '=': k = Tok::Equals; break;
-                case '|': k = Tok::Pipe; break;
-                case ':': k = Tok::Colon; break;
-                default:
-                    if (std::isalpha(static_cast<unsigned char>(c))) {
-                        std::size_t start = pos_;
-                        while (pos_ < src_.size() && (std::isalnum(static_cast<unsigned char>(src_[pos_])) || src_[pos_] == '_'))
-                            bump();
-                        tok_.kind = Tok::Ident;
-                        tok_.text = src_.substr(start, pos_ - start);
-                        tok_.span.length = static_cast<std::uint32_t>(pos_ - start);
-                        return;
-                    }
-                    errors_.push_back({tok_.span, ErrorKind::Lex, std::string("unexpected character '") + c + "'"});
-                    bump();
-                    continue;  // resynchronise on the next token
-            }
-            tok_.kind = k;
-            tok_.text = src_.substr(pos_, 1);
-            bump();
-            return;
+            default:
+                errors.push_back({{line, col, 1}, ErrorKind::Lex, std::string("unexpected character '") + src[i] + "'"});
+                advance(1);
+                break;
         }
     }
-
-    std::string_view src_;
-    std::vector<ParseError>& errors_;
-    std::size_t pos_ = 0;
-    std::uint32_t line_ = 1, col_ = 1;
-    Token tok_;
-};
+    out.push_back({Tok::End, {}, {line, col, 1}});
+    return out;
+}
 
 // Raw (unresolved) term: flat nodes in post-order; kids index into `kids`.
 struct RawNode {
@@ -164,242 +182,187 @@ struct RawSpec {
     RawTerm input;
 };
 
-class Parser {
+// ---- statement parser ------------------------------------------------------
+// Grammar (the reference's language; proj/src/parser.cpp):
+//   file   := 'sort' sortdecl* 'var' vardecl* 'eqn' eqn* ('input'|'Input') term ';'
+//   sortdecl := NAME '=' ['struct'] ctor ('|' ctor)* ';'
+//   ctor   := NAME '(' [NAME (',' NAME)*] ')'
+//   vardecl := NAME ':' NAME ';'
+//   eqn    := term '=' term ';'
+//   term   := NAME ['(' [term (',' term)*] ')']
+// A statement with an error is reported once, at the first offending
+// token, and dropped: parsing resumes after the next ';' or at the next
+// keyword (the statement cannot extend past either), and its section goes on
+// with the next statement.  A section runs while the next statement starts
+// with a name.  Diagnostics are the reference's, word for word
+// (tests/test_host.py compares them with parser.cpp's).
+
+class StatementParser {
 public:
-    Parser(std::string_view text, std::vector<ParseError>& errors) : errors_(errors), lex_(text, errors) {}
+    StatementParser(std::string_view text, std::vector<ParseError>& errors)
+        : toks_(scan(text, errors)), errors_(errors) {}
 
     std::optional<RawSpec> run() {
         RawSpec spec;
-        if (!section("sort")) return std::nullopt;
-        sorts(spec);
-        if (!section("var")) return std::nullopt;
-        vars(spec);
-        if (!section("eqn")) return std::nullopt;
-        eqns(spec);
-        if (!at("input") && !at("Input")) {
-            error(lex_.peek().span, ErrorKind::Syntax, "missing required sections: expected 'input'");
-            return std::nullopt;
+        using Stmt = bool (StatementParser::*)(RawSpec&);
+        const std::pair<std::string_view, Stmt> sections[] = {
+            {"sort", &StatementParser::sort_decl}, {"var", &StatementParser::var_decl}, {"eqn", &StatementParser::eqn}};
+        for (const auto& [keyword, stmt] : sections) {
+            if (!keyword_at(pos_, keyword)) return missing(keyword);
+            ++pos_;
+            while (name_at(pos_))
+                if (!(this->*stmt)(spec)) resync();
         }
-        lex_.take();
+        if (!keyword_at(pos_, "input") && !keyword_at(pos_, "Input")) return missing("input");
+        ++pos_;
         term(spec.input);
         expect(Tok::Semi, "';'");
-        if (lex_.peek().kind != Tok::End)
-            error(lex_.peek().span, ErrorKind::Syntax, "trailing input after 'input' section");
+        if (toks_[pos_].kind != Tok::End)
+            report(toks_[pos_].span, ErrorKind::Syntax, "trailing input after 'input' section");
         if (!errors_.empty()) return std::nullopt;
         return spec;
     }
 
 private:
-    bool at(std::string_view w) const { return lex_.peek().kind == Tok::Ident && lex_.peek().text == w; }
-    bool at_name() const { return lex_.peek().kind == Tok::Ident && !reserved(lex_.peek().text); }
-    void error(SourceSpan s, ErrorKind k, std::string m) { errors_.push_back({s, k, std::move(m)}); }
-    std::string context() const {
-        const Token& t = lex_.peek();
-        return t.kind == Tok::End ? " before end of input" : " before '" + std::string(t.text) + "'";
-    }
-    bool section(std::string_view kw) {
-        if (at(kw)) {
-            lex_.take();
-            return true;
+    // after an error: past the statement's ';', or up to a keyword or the end
+    void resync() {
+        for (; toks_[pos_].kind != Tok::End; ++pos_) {
+            if (toks_[pos_].kind == Tok::Semi) {
+                ++pos_;
+                return;
+            }
+            if (toks_[pos_].kind == Tok::Ident && reserved(toks_[pos_].text)) return;
         }
-        error(lex_.peek().span, ErrorKind::Syntax, "missing required sections: expected '" + std::string(kw) + "'");
+    }
+    bool keyword_at(std::size_t i, std::string_view w) const {
+        return toks_[i].kind == Tok::Ident && toks_[i].text == w;
+    }
+    bool name_at(std::size_t i) const { return toks_[i].kind == Tok::Ident && !reserved(toks_[i].text); }
+    std::optional<RawSpec> missing(std::string_view keyword) {
+        report(toks_[pos_].span, ErrorKind::Syntax, "missing required sections: expected '" + std::string(keyword) + "'");
+        return std::nullopt;
+    }
+    void report(SourceSpan at, ErrorKind kind, std::string message) {
+        errors_.push_back({at, kind, std::move(message)});
+    }
+    // an error at the current token, with the reference's " before ..." tail
+    bool fail(std::string what) {
+        const Token& t = toks_[pos_];
+        report(t.span, ErrorKind::Syntax,
+               what + (t.kind == Tok::End ? " before end of input" : " before '" + std::string(t.text) + "'"));
         return false;
     }
     bool expect(Tok k, const char* what) {
-        if (lex_.peek().kind == k) {
-            lex_.take();
+        if (toks_[pos_].kind == k) {
+            ++pos_;
             return true;
         }
-        error(lex_.peek().span, ErrorKind::Syntax, std::string("expected ") + what + context());
-        return false;
+        return fail(std::string("expected ") + what);
     }
-    void skip_statement() {
-        for (;;) {
-            const Token& t = lex_.peek();
-            if (t.kind == Tok::End) return;
-            if (t.kind == Tok::Semi) {
-                lex_.take();
-                return;
-            }
-            if (t.kind == Tok::Ident && reserved(t.text)) return;
-            lex_.take();
-        }
+    bool accept(Tok k) {
+        if (toks_[pos_].kind != k) return false;
+        ++pos_;
+        return true;
     }
 
-    void sorts(RawSpec& spec) {
-        while (at_name()) {
-            RawSort decl;
-            Token name = lex_.take();
-            decl.name = std::string(name.text);
-            decl.span = name.span;
-            if (!expect(Tok::Equals, "'='")) {
-                skip_statement();
-                continue;
+    bool sort_decl(RawSpec& spec) {
+        RawSort decl;
+        decl.name = std::string(toks_[pos_].text);
+        decl.span = toks_[pos_++].span;
+        if (!expect(Tok::Equals, "'='")) return false;
+        if (keyword_at(pos_, "struct")) ++pos_;
+        do {
+            if (!name_at(pos_)) return fail("expected constructor name");
+            RawCtor ctor;
+            ctor.name = std::string(toks_[pos_].text);
+            ctor.span = toks_[pos_++].span;
+            if (!expect(Tok::LParen, "'(' (constants are written with explicit '()')")) return false;
+            if (toks_[pos_].kind != Tok::RParen) {
+                do {
+                    if (toks_[pos_].kind != Tok::Ident) return fail("expected sort name");
+                    ctor.arg_sorts.emplace_back(std::string(toks_[pos_].text), toks_[pos_].span);
+                    ++pos_;
+                } while (accept(Tok::Comma));
             }
-            if (at("struct")) lex_.take();
-            bool ok = true;
-            for (;;) {
-                if (!at_name()) {
-                    error(lex_.peek().span, ErrorKind::Syntax, "expected constructor name" + context());
-                    ok = false;
-                    break;
-                }
-                RawCtor ctor;
-                Token cn = lex_.take();
-                ctor.name = std::string(cn.text);
-                ctor.span = cn.span;
-                if (!expect(Tok::LParen, "'(' (constants are written with explicit '()')")) {
-                    ok = false;
-                    break;
-                }
-                bool arg_ok = true;
-                if (lex_.peek().kind != Tok::RParen) {
-                    for (;;) {
-                        if (lex_.peek().kind != Tok::Ident) {
-                            error(lex_.peek().span, ErrorKind::Syntax, "expected sort name" + context());
-                            arg_ok = false;
-                            break;
-                        }
-                        Token s = lex_.take();
-                        ctor.arg_sorts.emplace_back(std::string(s.text), s.span);
-                        if (lex_.peek().kind == Tok::Comma) {
-                            lex_.take();
-                            continue;
-                        }
-                        break;
-                    }
-                }
-                if (!arg_ok || !expect(Tok::RParen, "')'")) {
-                    ok = false;
-                    break;
-                }
-                decl.ctors.push_back(std::move(ctor));
-                if (lex_.peek().kind == Tok::Pipe) {
-                    lex_.take();
-                    continue;
-                }
-                break;
-            }
-            if (!ok || !expect(Tok::Semi, "';'")) {
-                skip_statement();
-                continue;
-            }
-            spec.sorts.push_back(std::move(decl));
-        }
+            if (!expect(Tok::RParen, "')'")) return false;
+            decl.ctors.push_back(std::move(ctor));
+        } while (accept(Tok::Pipe));
+        if (!expect(Tok::Semi, "';'")) return false;
+        spec.sorts.push_back(std::move(decl));
+        return true;
     }
 
-    void vars(RawSpec& spec) {
-        while (at_name()) {
-            RawVar v;
-            Token name = lex_.take();
-            v.name = std::string(name.text);
-            v.span = name.span;
-            if (!expect(Tok::Colon, "':'")) {
-                skip_statement();
-                continue;
-            }
-            if (lex_.peek().kind != Tok::Ident) {
-                error(lex_.peek().span, ErrorKind::Syntax, "expected sort name" + context());
-                skip_statement();
-                continue;
-            }
-            Token s = lex_.take();
-            v.sort = std::string(s.text);
-            v.sort_span = s.span;
-            if (!expect(Tok::Semi, "';'")) {
-                skip_statement();
-                continue;
-            }
-            spec.vars.push_back(std::move(v));
-        }
+    bool var_decl(RawSpec& spec) {
+        RawVar v;
+        v.name = std::string(toks_[pos_].text);
+        v.span = toks_[pos_++].span;
+        if (!expect(Tok::Colon, "':'")) return false;
+        if (toks_[pos_].kind != Tok::Ident) return fail("expected sort name");
+        v.sort = std::string(toks_[pos_].text);
+        v.sort_span = toks_[pos_++].span;
+        if (!expect(Tok::Semi, "';'")) return false;
+        spec.vars.push_back(std::move(v));
+        return true;
     }
 
-    void eqns(RawSpec& spec) {
-        while (at_name()) {
-            RawEqn e;
-            if (!term(e.lhs)) {
-                skip_statement();
-                continue;
-            }
-            if (!expect(Tok::Equals, "'='")) {
-                skip_statement();
-                continue;
-            }
-            if (!term(e.rhs)) {
-                skip_statement();
-                continue;
-            }
-            if (!expect(Tok::Semi, "';'")) {
-                skip_statement();
-                continue;
-            }
-            spec.eqns.push_back(std::move(e));
-        }
+    bool eqn(RawSpec& spec) {
+        RawEqn e;
+        if (!term(e.lhs) || !expect(Tok::Equals, "'='") || !term(e.rhs) || !expect(Tok::Semi, "';'")) return false;
+        spec.eqns.push_back(std::move(e));
+        return true;
     }
 
-    // IDENT [ '(' term (',' term)* ')' ] with an explicit frame stack.
+    // term := NAME ['(' [term (',' term)*] ')'], with an explicit frame stack
+    // (terms nest as deep as the input); nodes are emitted in post-order.
     bool term(RawTerm& out) {
-        struct Open {
-            std::string_view name;
-            SourceSpan span;
+        struct Frame {
+            std::uint32_t tok;               // the applied name
             std::vector<std::uint32_t> kids;
         };
-        std::vector<Open> open;
-        auto finish = [&](std::string_view name, bool has_args, SourceSpan span, const std::vector<std::uint32_t>& kids) {
+        std::vector<Frame> frames;
+        auto emit = [&](std::uint32_t tok, bool has_args, const std::vector<std::uint32_t>& kids) {
             RawNode n;
-            n.name = name;
+            n.name = toks_[tok].text;
             n.has_args = has_args;
-            n.span = span;
+            n.span = toks_[tok].span;
             n.first = static_cast<std::uint32_t>(out.kids.size());
             n.count = static_cast<std::uint32_t>(kids.size());
             out.kids.insert(out.kids.end(), kids.begin(), kids.end());
             out.nodes.push_back(n);
             return static_cast<std::uint32_t>(out.nodes.size() - 1);
         };
-        static const std::vector<std::uint32_t> none;
         for (;;) {
-            if (!at_name()) {
-                error(lex_.peek().span, ErrorKind::Syntax, "expected a term" + context());
-                return false;
-            }
-            Token name = lex_.take();
+            // an operand: a name, a constant `Name()`, or the opening of an application
+            if (!name_at(pos_)) return fail("expected a term");
+            const std::uint32_t tok = static_cast<std::uint32_t>(pos_++);
             std::uint32_t node;
-            if (lex_.peek().kind == Tok::LParen) {
-                lex_.take();
-                if (lex_.peek().kind != Tok::RParen) {
-                    open.push_back({name.text, name.span, {}});
+            if (accept(Tok::LParen)) {
+                if (!accept(Tok::RParen)) {
+                    frames.push_back({tok, {}});
                     continue;
                 }
-                lex_.take();
-                node = finish(name.text, true, name.span, none);
+                node = emit(tok, true, {});
             } else {
-                node = finish(name.text, false, name.span, none);
+                node = emit(tok, false, {});
             }
+            // close the applications this operand completes
             for (;;) {
-                if (open.empty()) {
+                if (frames.empty()) {
                     out.root = node;
                     return true;
                 }
-                open.back().kids.push_back(node);
-                if (lex_.peek().kind == Tok::Comma) {
-                    lex_.take();
-                    break;
-                }
-                if (lex_.peek().kind == Tok::RParen) {
-                    lex_.take();
-                    Open f = std::move(open.back());
-                    open.pop_back();
-                    node = finish(f.name, true, f.span, f.kids);
-                    continue;
-                }
-                error(lex_.peek().span, ErrorKind::Syntax, "expected ',' or ')' in argument list" + context());
-                return false;
+                frames.back().kids.push_back(node);
+                if (accept(Tok::Comma)) break;
+                if (!accept(Tok::RParen)) return fail("expected ',' or ')' in argument list");
+                node = emit(frames.back().tok, true, frames.back().kids);
+                frames.pop_back();
             }
         }
     }
 
+    std::vector<Token> toks_;
     std::vector<ParseError>& errors_;
-    Lexer lex_;
+    std::size_t pos_ = 0;
 };
 
 class Resolver {
@@ -624,7 +587,7 @@ private:
 
 ResolveResult load_system(std::string_view text) {
     std::vector<ParseError> errors;
-    Parser parser(text, errors);
+    StatementParser parser(text, errors);
     std::optional<RawSpec> spec = parser.run();
     if (!spec || !errors.empty()) {
         ResolveResult r;

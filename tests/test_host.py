@@ -158,3 +158,47 @@ def test_batched_store_rejects_mismatched_signatures():
 def test_print_words_round_trip():
     s = api.System(W.fib(5))
     assert s.print_words(s.input_canonical()) == s.print_input() == f"Fib({W.peano(5)})"
+
+
+def _mutants(seed: int):
+    """Syntax-error mutants of valid systems: a punctuation or word removed,
+    doubled or swapped for another, anywhere in the text."""
+    import random
+    import re
+
+    rng = random.Random(seed)
+    base = [W.fib(3), W.mergesort(3, 1), W.buildsum(2), W.ackermann(1, 1),
+            "sort T = struct A() | F(T) | G(T, T);\nvar X : T; Y : T;\neqn F(X) = G(X, X);\ninput F(A());\n"]
+    text = rng.choice(base)
+    toks = [m for m in re.finditer(r"[A-Za-z_][A-Za-z0-9_]*|[(),;=|:%$]", text)]
+    out = []
+    for _ in range(4):
+        m = rng.choice(toks)
+        a, b = m.span()
+        op = rng.randrange(4)
+        if op == 0:
+            t = text[:a] + text[b:]
+        elif op == 1:
+            t = text[:a] + m.group() + " " + text[a:]
+        elif op == 2:
+            t = text[:a] + rng.choice(["(", ")", ",", ";", "=", "|", ":", "sort", "var", "eqn", "input", "struct",
+                                       "Q", "$", "%"]) + text[b:]
+        else:
+            c = rng.choice(toks)
+            t = text[:a] + c.group() + text[b:]
+        out.append(t)
+    return out
+
+
+@pytest.mark.skipif(not ref.available(), reason="oracle/_ref not built here")
+@pytest.mark.parametrize("seed", range(150))
+def test_diagnostics_fuzz_match_reference(seed):
+    """Error recovery equals the reference's on mutated systems: the same
+    located diagnostics, in the same order, or the same acceptance."""
+    for text in _mutants(seed):
+        try:
+            api.System(text)
+            ours = ""
+        except ValueError as e:
+            ours = str(e)
+        assert ours == ref.diagnostics(text), text
