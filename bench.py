@@ -618,7 +618,7 @@ def main():
                                        "flatten_to_soa": round(1e3 * (t_in2 - t_in1), 1)}},
         "gpu_launches": launches,
         "clocks": clocks.summary(),
-        "parity": parity, "parity_all_ranks": bool(all_ok), "rewrites_all_ranks": int(all_rw),
+        "parity": parity, "parity_all_ranks": bool(all_ok), "rewrites_all_ranks": int(all_rw / args.steps),
         "engine": {"sweeps": stats[-1]["sweeps"], "small_sweeps": stats[-1]["small_sweeps"],
                    "gc_runs": stats[-1]["gc_runs"], "grid_blocks": stats[-1]["grid_blocks"],
                    "block_threads": stats[-1]["block_threads"], "record_words": stats[-1]["record_words"],

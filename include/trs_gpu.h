@@ -106,7 +106,11 @@ typedef struct trs_gpu_program {
 typedef struct trs_gpu_options {
     uint64_t step_budget;      /* 0 -> 1e9 (sweep_engine.hpp:32) */
     uint32_t fixed_capacity;   /* 1: never grow; CAPACITY when the arena fills */
-    uint32_t validate;         /* 1: check the refcount ghost invariant after the run */
+    uint32_t validate;         /* 1: check the refcount ghost invariant after the run; 2: also scan the whole
+                                  store before every sweep (ghost refcounts, dangling references, nf
+                                  monotonicity, inner-most safety, garbage is nf, no lost slot; grid mode
+                                  only), the reference's validate mode (sweep_engine.cpp:307-379);
+                                  violations: TRS_GPU_DANGLING */
     uint32_t small_enter;      /* frontier size at/below which one CTA runs the sweeps (0 -> default) */
     uint32_t small_exit;       /* frontier size above which the whole grid takes over again */
     uint32_t disable_small;    /* 1: never use single-CTA mode */

@@ -34,6 +34,7 @@ enum Status : uint32_t {
     kCapacity = 3,
     kNeedGrow = 4,
     kNeedTrace = 5,
+    kValidate = 6,   // a validate=2 scan found a violation (Ctl::val_kind)
 };
 
 // Control block in device memory.  Persistent fields are written by one
@@ -73,6 +74,7 @@ struct Ctl {
     uint32_t need_hist;       // a slot's derive sweep lies past the width histogram
     uint32_t hist_need;       // the histogram entries it needs
     uint32_t ra_narrow, ra_on, ra_used;  // run-ahead state (sweep.cuh, ra_track)
+    uint32_t val_kind, val_slot;         // first validate=2 violation (validate.cuh)
     // phase cycle accounting (Params::profile): match, claim, apply, push,
     // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
     // the match sub-phases: record, children, slots, rules
@@ -129,6 +131,8 @@ struct Params {
     uint32_t ra_steps;      // consecutive run-ahead steps of a lane before it pushes instead (a long
                             // chain must not hold back the work its steps pushed to the next sweep)
     uint64_t list_cap;      // entries per frontier list buffer
+    uint32_t validate;      // 2: quiescent-point scans before every grid sweep (validate.cuh)
+    uint32_t* val;          // their scratch, 3 words per slot
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

@@ -189,6 +189,8 @@ __global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t* region_flags
             c->ra_narrow = 0;
             c->ra_on = 0;
             c->ra_used = 0;
+            c->val_kind = 0;
+            c->val_slot = 0;
         }
         c->status = kRunning;
         c->bar_arrive = 0;
@@ -342,6 +344,8 @@ struct trs_gpu_engine {
     uint32_t hist_cap = 0;
     uint32_t hist_used = 0;                   // entries the last run wrote (zeroed before the next)
     uint32_t* d_region_flags = nullptr;       // [2][kMaxGrid]
+    uint32_t* d_val = nullptr;                // validate=2 scratch (validate.cuh), 3 words per slot
+    uint64_t val_cap = 0;
     uint32_t last_psweeps = 0;
     bool loaded = false;
     uint32_t last_sweeps = 0;
@@ -389,6 +393,9 @@ void free_store(trs_gpu_engine* e) {
     cudaFree(e->d_trace);
     cudaFree(e->d_hist);
     cudaFree(e->d_region_flags);
+    cudaFree(e->d_val);
+    e->d_val = nullptr;
+    e->val_cap = 0;
     e->d_hist = nullptr;
     e->d_region_flags = nullptr;
     e->hist_cap = e->hist_used = 0;
@@ -1328,6 +1335,22 @@ int enqueue_launch(trs_gpu_engine* e) {
     // time keeps the widths exact) except where the reference's abort state
     // is part of the contract: an explicit step budget or a fixed capacity
     P.runahead = (R.runahead && !e->rich) ? 1u : 0u;
+    if (opt.validate >= 2) {
+        // quiescent-point scans before every grid sweep (validate.cuh): the
+        // whole run in the grid mode, no run-ahead
+        if (e->val_cap < e->alloc_capacity) {
+            cudaFree(e->d_val);
+            e->d_val = nullptr;
+            e->val_cap = 0;
+            CUDA_TRY(e, cudaMalloc(&e->d_val, sizeof(uint32_t) * 3 * e->alloc_capacity));
+            e->val_cap = e->alloc_capacity;
+        }
+        CUDA_TRY(e, cudaMemsetAsync(e->d_val, 0, sizeof(uint32_t) * 3 * e->val_cap, e->stream));
+        P.validate = 2;
+        P.val = e->d_val;
+        P.small_enter = P.small_exit = 0;
+        P.runahead = 0;
+    }
     {
         const char* rm = std::getenv("TRS_B200_RA_MAX");  // tuning hook
         P.ra_max = rm ? (uint32_t)std::strtoul(rm, nullptr, 10) : (uint32_t)R.blocks * kWarps * 4u;
@@ -1445,6 +1468,17 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
             if (r) { result = r; break; }
             continue;
         }
+        if (c.status == kValidate) {
+            static const char* kinds[] = {"", "a live slot references slot 0, a slot past the store or a collected slot",
+                                          "refcount ghost invariant broken", "nf monotonicity: a slot left normal form",
+                                          "inner-most safety: an nf slot has an argument that was not nf before it",
+                                          "garbage that is not in normal form", "a live slot is neither on the frontier "
+                                          "nor subscribed to an argument"};
+            result = fail(e, TRS_GPU_DANGLING, std::string("sweep invariant violation: ") +
+                                                   kinds[c.val_kind < 7 ? c.val_kind : 0] + " (slot " +
+                                                   std::to_string(c.val_slot) + ")");
+            break;
+        }
         if (c.status == kNeedGrow) {
             uint64_t m = 0;
             const Ctl cg = c;
@@ -1474,7 +1508,9 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
     cudaGetLastError();
     e->last_sweeps = c.sweep - c.sweep0;
     e->last_psweeps = c.psweep;
-    e->hist_used = std::min<uint32_t>(e->hist_cap, e->last_sweeps);
+    // a completed run rewrote only in sweeps up to its last nf epoch; a run
+    // that stopped early (budget, capacity) may have counted rewrites past it
+    e->hist_used = result == TRS_GPU_OK ? std::min<uint32_t>(e->hist_cap, e->last_sweeps) : e->hist_cap;
     if (result == TRS_GPU_OK && opt.validate) result = validate_store(e);
     if (stats) *stats = st;
     return result;

@@ -20,6 +20,7 @@
 #pragma once
 
 #include "gc.cuh"
+#include "validate.cuh"
 
 namespace trs_b200 {
 
@@ -1625,9 +1626,22 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         return;
     }
 
+    bool val_monotone = false;  // the first scan of a launch (or after a collection) has no previous epochs
+    auto validate_now = [&]() -> bool {
+        // every slab's unused slots are marked collected before the scan
+        abandon_slab<W>(P.arena[L.arena], slab);
+        grid_sync(ctl, nblocks, epoch);
+        validate_store_device<W>(P, G, L.arena, L.bump, F, L.cur, blockIdx.x, nblocks, epoch, val_monotone);
+        val_monotone = true;
+        return __ldcg(&ctl->val_kind) == 0u;
+    };
     for (;;) {
         const uint32_t s = L.sweep + 1;
         const uint32_t m = F.M;
+        if (P.validate >= 2 && !validate_now()) {
+            exit_status = kValidate;
+            break;
+        }
         const uint32_t pl = plan(P, L, m, just_collected, nwarps);
         if (pl == kPlanFinish) {
             // the first sweep whose frontier is empty (sweep_engine.cpp:147)
@@ -1648,6 +1662,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             collect();
             L.last_gc = L.sweep + 1;
             just_collected = true;
+            val_monotone = false;  // slots were renumbered
             continue;
         }
 

@@ -120,7 +120,8 @@ def _pad_add(a, b):
                                   dict(disable_small=1, gc_interval=3), dict(blocks_per_sm=1, small_enter=4),
                                   dict(profile=1), dict(disable_warp_mode=1, max_blocks=3), dict(disable_gc=1),
                                   dict(small_enter=40, small_exit=40), dict(validate=1, gc_interval=1),
-                                  dict(no_runahead=1), dict(no_runahead=1, disable_small=1)])
+                                  dict(no_runahead=1), dict(no_runahead=1, disable_small=1),
+                                  dict(validate=2), dict(validate=2, gc_interval=2)])
 @pytest.mark.parametrize("name", ["treemergesort_4_5_s7", "fibbatch64_s3", "unit_two_waiters", "transform6"])
 def test_knobs_do_not_change_results(engine, name, opts):
     g = CASES[name]
@@ -418,7 +419,7 @@ def test_slab_size_does_not_change_results(engine, name, slab):
     np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
 
 
-@pytest.mark.parametrize("mode", ["default", "grid_only", "no_warp", "gc1", "interp", "no_runahead"])
+@pytest.mark.parametrize("mode", ["default", "grid_only", "no_warp", "gc1", "interp", "no_runahead", "validate2"])
 @pytest.mark.parametrize("seed", range(40))
 def test_random_programs_against_oracle(engine, seed, mode):
     """Random terminating systems (workloads.random_program; the oracle
@@ -429,7 +430,8 @@ def test_random_programs_against_oracle(engine, seed, mode):
     text = W.random_program(seed)
     o = port.run_text(text)
     opts = {"default": {}, "grid_only": {"disable_small": 1}, "no_warp": {"disable_warp_mode": 1},
-            "gc1": {"gc_interval": 1, "validate": 1}, "interp": {}, "no_runahead": {"no_runahead": 1}}[mode]
+            "gc1": {"gc_interval": 1, "validate": 1}, "interp": {}, "no_runahead": {"no_runahead": 1},
+            "validate2": {"validate": 2, "gc_interval": 3}}[mode]
     opt = api.make_options(**opts)
     if mode == "interp":
         opt.reserved[1] = 2
@@ -519,3 +521,43 @@ def test_random_program_export(engine, seed, gc_interval):
     assert (counted[1:] > 0).all() and out["nf"][1:n].all()
     for k in range(len(texts)):
         np.testing.assert_array_equal(engine.canonical(k), o.words[k])
+
+
+def test_validate2_reports_a_corrupted_store(engine):
+    """validate=2 scans the store before the first sweep: a live slot whose
+    argument is slot 0 is a sweep invariant violation (sweep_engine.cpp:
+    341-344), reported as DanglingReference before any rewriting."""
+    s = api.System(W.mergesort(2).split("input ")[0] + "input Cons(Zero(), Cons(Zero(), Nil()));\n")
+    st = api.Store.load(s)
+    st.poke_arg(1, 1, 0)
+    engine.set_program(s)
+    engine.load(st)
+    with pytest.raises(api.EngineError) as ei:
+        engine.run(api.make_options(validate=2))
+    assert ei.value.fault == api.EngineFault.DanglingReference
+    assert "sweep invariant violation" in str(ei.value)
+
+
+@pytest.mark.parametrize("name", ["fibbatch_s1", "sortbatch_s1"])
+def test_validate2_full_size_shard(engine, name):
+    """The per-sweep device scans on a full-size config 5 shard (1,293 /
+    982 scans of a multi-million-slot store) find nothing, and the run's
+    results are the reference's."""
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fullsize_ref.json")))[name]
+    text = W.fib_batch(1) if name.startswith("fib") else W.treemergesort_batch(1)
+    res = api.normalize_texts(text, engine=engine, options=api.make_options(validate=2))
+    assert res.total_rewrites == fx["rewrites"] and res.sweeps == fx["sweeps"]
+    assert hashlib.sha1(res.widths.astype("<u8").tobytes()).hexdigest() == fx["widths_sha1"]
+
+
+@pytest.mark.parametrize("budget", [10, 100, 1000])
+def test_widths_clean_after_a_stopped_run(engine, budget):
+    """A run stopped by its step budget has counted rewrites in sweeps past
+    its last nf epoch; the next run on the same engine must not inherit them
+    (the width histogram is cleared over everything the stopped run may have
+    written)."""
+    g = CASES["fib12"]
+    with pytest.raises(api.EngineError):
+        api.normalize_texts(g["text"], engine=engine, options=api.make_options(step_budget=budget))
+    res = api.normalize_texts(g["text"], engine=engine)
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
