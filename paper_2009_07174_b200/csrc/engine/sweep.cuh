@@ -60,10 +60,10 @@ __device__ __forceinline__ void abandon_slab(uint32_t* arena, Slab& slab) {
 // logical sweep (flushed once per CTA and sweep): every warp of a wide sweep
 // hitting the same global entry would serialise in one L2 slice.
 constexpr uint32_t kHistWin = 32;
-template <bool kSolo>
-__device__ __forceinline__ void hist_add(unsigned long long* h, bool on) {
+template <bool kSolo, typename Ctr>
+__device__ __forceinline__ void hist_add(Ctr* h, bool on) {
     if (kSolo) {
-        if (on) atomicAdd(h, 1ull);
+        if (on) atomicAdd(h, (Ctr)1);
         return;
     }
     const uint32_t act = __ballot_sync(0xffffffffu, on);
@@ -73,7 +73,7 @@ __device__ __forceinline__ void hist_add(unsigned long long* h, bool on) {
     const unsigned long long lead = __shfl_sync(0xffffffffu, mine, first);
     const uint32_t same = __ballot_sync(0xffffffffu, on && mine == lead);
     const int lane = threadIdx.x & 31;
-    if (on && (mine != lead || lane == first)) atomicAdd(h, mine != lead ? 1ull : (unsigned long long)__popc(same));
+    if (on && (mine != lead || lane == first)) atomicAdd(h, mine != lead ? (Ctr)1 : (Ctr)__popc(same));
 }
 
 // Warp collectives of the warp step, or their one-lane identities when a
@@ -103,7 +103,7 @@ struct StepCtx {
     uint32_t t0;          // the run's first logical sweep (earliest sweep of an input slot)
     unsigned long long* hist;
     uint32_t hist_cap;
-    unsigned long long* hwin;  // CTA-shared width window [hbase, hbase + kHistWin) (null: global adds)
+    uint32_t* hwin;       // CTA-shared width window [hbase, hbase + kHistWin) (null: global adds)
     uint32_t hbase;
     uint32_t stamp;       // physical sweep mod 16, published with nf epochs
     uint32_t ra;          // the run may run ahead: readiness by stamps, not by sweep number
@@ -1560,7 +1560,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     __shared__ uint32_t s_push;
     __shared__ uint32_t s_flags;
     __shared__ int s_cont;
-    __shared__ unsigned long long s_hwin[kHistWin];
+    __shared__ uint32_t s_hwin[kHistWin];
     // stage the program tables; the single-CTA frontier lists follow them
     for (uint32_t o = threadIdx.x * 16; o < P.prog_bytes; o += kBlock * 16)
         *reinterpret_cast<uint4*>(smem_raw + o) = *reinterpret_cast<const uint4*>(P.prog + o);
@@ -1709,7 +1709,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             s_flags = 0;
             s_cont = (int)slack;
         }
-        if (threadIdx.x < kHistWin) s_hwin[threadIdx.x] = 0ull;
+        if (threadIdx.x < kHistWin) s_hwin[threadIdx.x] = 0u;
         __syncthreads();
         const uint32_t out_off =
             (P.max_new + 1) * cta_prefix(m, blockIdx.x, nblocks, chunk_lanes(m, nblocks)) + blockIdx.x * slack;
@@ -1752,7 +1752,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
 #endif
         rw = block_sum64(rw, sm);  // ends synchronised: the width window is complete
         if (threadIdx.x < kHistWin && s_hwin[threadIdx.x])
-            atomicAdd(P.hist + (C.hbase - C.t0 + threadIdx.x), s_hwin[threadIdx.x]);
+            atomicAdd(P.hist + (C.hbase - C.t0 + threadIdx.x), (unsigned long long)s_hwin[threadIdx.x]);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
             region_cnt(P, L.cur ^ 1)[blockIdx.x] = s_push;

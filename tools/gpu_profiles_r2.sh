@@ -1,0 +1,19 @@
+#!/bin/bash
+# round-2 profiles: bench line, reference arm, launch list, ncu --set full of the step loop per config and of
+# the export, canonical relabelling and gather probe kernels
+cd "${GRAFT_REPO_ROOT:-.}"
+mkdir -p gpurun_out
+timeout 900 python bench.py > gpurun_out/bench_full.json 2> gpurun_out/bench_full.err; echo "bench rc=$?"
+timeout 300 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.json 2>&1; echo "ref rc=$?"
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv \
+    python bench.py --steps 2 --warmup 3 --no-configs --no-cpu-baseline --no-gate > /dev/null 2>&1; echo "launches rc=$?"
+for c in fibbatch transform22 fib18 sortbatch buildsum22 fibbatch1; do
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:step_loop -s 1 -c 1 \
+      -o gpurun_out/ncu_$c python tools/profile_target.py $c > gpurun_out/ncu_$c.log 2>&1; echo "ncu $c rc=$?"
+done
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:export_store -c 1 \
+    -o gpurun_out/ncu_export python tools/e2e_parts.py > gpurun_out/ncu_export.log 2>&1; echo "ncu export rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:canon_down -c 1 \
+    -o gpurun_out/ncu_canon python tools/canon_target.py > gpurun_out/ncu_canon.log 2>&1; echo "ncu canon rc=$?"
+timeout 600 ncu --set full --clock-control none -k regex:gather_probe -s 1 -c 1 \
+    -o gpurun_out/ncu_probe python tools/probe_target.py > gpurun_out/ncu_probe.log 2>&1; echo "ncu probe rc=$?"

@@ -19,22 +19,35 @@ WANT = ['gpu__time_duration.sum', 'dram__bytes_read.sum', 'dram__bytes_write.sum
 NAMES = {"fibbatch": ("config 5F fib batch, 8 shards", "fibbatch_8shards"),
          "sortbatch": ("config 5S tree-merge-sort batch, 8 shards", "sortbatch_8shards"),
          "buildsum22": ("config 3b build+sum depth 22", "buildsum22"),
-         "export": ("normal-form export of config 5F (trs_gpu_fetch_store)", "export_fibbatch_8shards")}
+         "transform22": ("config 3a transform depth 22", "transform22"),
+         "fib18": ("config 1 fib(18)", "fib18"),
+         "fibbatch1": ("config 5F, one shard (the strong-scaling 8-GPU point)", "fibbatch_1shard"),
+         "export": ("normal-form export of config 5F (trs_gpu_fetch_store)", "export_fibbatch_8shards"),
+         "canon": ("device canonical relabelling of config 5F (canon_down)", "canon_fibbatch_8shards"),
+         "probe": ("random 4-byte gather probe over 4 GiB (the roofline)", "gather_probe_4B_4GiB")}
 SCALE = {'Gbyte': 1e9, 'Mbyte': 1e6, 'Kbyte': 1e3, 'byte': 1}
 
 
 def main():
     src = sys.argv[1] if len(sys.argv) > 1 else os.path.join(ROOT, "gpurun_out")
-    out = ["# Round 1 ncu summaries (specialised step loop): ncu --set full --clock-control none --import-source on",
-           "# one steady-state launch each; captured with tools/gpu_profiles.sh, summarised by tools/ncu_summary.py",
+    tag = sys.argv[2] if len(sys.argv) > 2 else "r1"
+    out = [f"# {tag} ncu summaries (specialised step loop): ncu --set full --clock-control none --import-source on",
+           "# one steady-state launch each; captured with tools/gpu_profiles*.sh, summarised by tools/ncu_summary.py",
            "#   step_loop: python tools/profile_target.py <workload>   (-k regex:step_loop -s 1 -c 1)",
            "#   export_store: python tools/e2e_parts.py                (-k regex:export_store -c 1)",
            "# ncu times are replayed/serialised: compare shares, not absolutes", ""]
     traffic = {}
+    if os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)
     for c, (desc, key) in NAMES.items():
-        r = subprocess.run(["ncu", "-i", os.path.join(src, f"ncu_{c}.ncu-rep"), "--page", "raw", "--csv"],
-                           capture_output=True, text=True).stdout
+        rep = os.path.join(src, f"ncu_{c}.ncu-rep")
+        if not os.path.exists(rep):
+            continue
+        r = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         rows = list(csv.reader(r.splitlines()))
+        if len(rows) < 3:
+            continue
         h, u, v = rows[0], rows[1], rows[2]
         out.append(f"## {c}: {desc}  ({v[h.index('Kernel Name')]})")
         for w in WANT:
@@ -45,7 +58,7 @@ def main():
         out.append(f"{'dram bytes per launch (read+write)':80s} {rd + wr:22.4e} byte")
         out.append("")
         traffic[key] = rd + wr
-    with open(os.path.join(ROOT, "profiles", "r1_ncu_summary.txt"), "w") as f:
+    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w") as f:
         f.write("\n".join(out))
     with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
