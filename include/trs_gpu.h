@@ -268,6 +268,16 @@ int trs_gpu_dump_program(trs_gpu_engine* engine, const char* const* symbol_names
                          const uint32_t* rule_var_begin, const uint32_t* rule_vars, const char* const* rule_texts,
                          char* out, uint64_t cap, uint64_t* need);
 
+/* Layout evidence: one pass of the derive's probe pattern (a slot's head,
+ * epoch word and arguments, then each argument's head and epoch word) over
+ * every slot of the current store, read from the engine's 8-word AoS records
+ * (layout 0) or from SoA columns built from them, the reference TermStore
+ * layout (layout 1).  Reports ms per pass (CUDA events, `iters` passes) and
+ * the slots scanned; ncu on trs_gpu_layout_probe's kernels gives the DRAM
+ * bytes and sectors of each layout. */
+int trs_gpu_layout_probe(trs_gpu_engine* engine, uint32_t layout, uint32_t iters, double* ms_per_pass,
+                         uint64_t* nodes);
+
 /* Exact count of slots with refcount > 0 in the current store: the
  * reference's live_terms (sweep_engine.cpp:122-123), which includes
  * garbage not yet collected. */

@@ -132,6 +132,7 @@ def lib():
         "trs_gpu_fetch_store": ([P, u32p, P, P, P, P, P, U32], I),
         "trs_gpu_canonical_all": ([P, P, U64, ctypes.POINTER(U64), P, P, P], I),
         "trs_gpu_live_count": ([P, ctypes.POINTER(U64)], I),
+        "trs_gpu_layout_probe": ([P, U32, U32, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(U64)], I),
         "trs_gpu_gather_probe": ([I, U64, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
         "trs_gpu_gather_probe_ex": ([I, U64, U32, U32, U32, ctypes.POINTER(ctypes.c_double)], I),
         "trs_gpu_stream": ([P], P),
@@ -176,7 +177,7 @@ def exported_symbols() -> list[str]:
                         "trs_gpu_last_error", "trs_gpu_set_program", "trs_gpu_load", "trs_gpu_load_device",
                         "trs_gpu_run", "trs_gpu_run_async", "trs_gpu_run_wait", "trs_gpu_hold",
                         "trs_gpu_release", "trs_gpu_jit_info", "trs_gpu_trace", "trs_gpu_canonical", "trs_gpu_fetch_store",
-                        "trs_gpu_canonical_all", "trs_gpu_live_count", "trs_gpu_phys_trace", "trs_gpu_gather_probe_ex",
+                        "trs_gpu_canonical_all", "trs_gpu_live_count", "trs_gpu_phys_trace", "trs_gpu_gather_probe_ex", "trs_gpu_layout_probe",
                         "trs_gpu_gather_probe", "trs_gpu_stream", "trs_gpu_compact", "trs_gpu_fetch_records",
                         "trs_gpu_profile_counters", "trs_gpu_overhead_probe")]
 
@@ -557,6 +558,13 @@ class Engine:
             _raise(rc, self._err())
             out["words"] = [flat[int(offs[k]):int(offs[k + 1])] for k in range(num_roots)]
         return out
+
+    def layout_probe(self, layout: int, iters: int = 5) -> dict:
+        """AoS (0) vs SoA (1) probe pass over the current store (trs_gpu_layout_probe)."""
+        ms = ctypes.c_double(0)
+        n = ctypes.c_uint64(0)
+        _raise(lib().trs_gpu_layout_probe(self._h, layout, iters, ctypes.byref(ms), ctypes.byref(n)), self._err())
+        return {"ms": ms.value, "slots": n.value}
 
     def live_count(self) -> int:
         """Slots with refcount > 0 (the reference's live_terms, sweep_engine.cpp:122-123)."""

@@ -35,6 +35,7 @@ enum Status : uint32_t {
     kNeedGrow = 4,
     kNeedTrace = 5,
     kValidate = 6,   // a validate=2 scan found a violation (Ctl::val_kind)
+    kNeedRA = 7,     // the lean build hands over to the run-ahead build
 };
 
 // Control block in device memory.  Persistent fields are written by one

@@ -246,6 +246,61 @@ __global__ void pack_store(const uint32_t* __restrict__ A, uint32_t n, const uin
     }
 }
 
+// Layout evidence: the derive's probe pattern -- a node's
+// head, epoch word and arguments, then each argument's head and epoch word --
+// over the store of the last run, read from the engine's AoS records or from
+// SoA columns built from them (the reference's TermStore layout,
+// term_store.hpp:15-45: hss, nf, args[j] as separate arrays).
+template <int W>
+__global__ void to_soa(const uint32_t* __restrict__ A, uint32_t n, uint32_t* __restrict__ hss,
+                       uint32_t* __restrict__ ep, uint32_t* __restrict__ args, uint32_t na) {
+    for (uint32_t y = blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+        const uint32_t* R = A + (size_t)y * W;
+        hss[y] = R[kWHead];
+        ep[y] = R[kWEpoch];
+        for (uint32_t j = 0; j < na; ++j) args[(size_t)j * n + y] = R[kWArgs + j];
+    }
+}
+
+template <int W>
+__global__ void probe_aos(const uint32_t* __restrict__ A, uint32_t n, const uint8_t* __restrict__ arity,
+                          uint32_t* __restrict__ sink) {
+    uint32_t acc = 0;
+    for (uint32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+        const uint4 h = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)y * W));
+        if (h.x == kDeadHead) continue;
+        const uint4 a = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)y * W + kWArgs));
+        const uint32_t ar = arity[h.x & kSymMask];
+        const uint32_t c[4] = {a.x, a.y, a.z, a.w};
+        acc += h.y;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if ((uint32_t)j < ar) {
+                const uint2 ch = __ldcg(reinterpret_cast<const uint2*>(A + (size_t)c[j] * W));
+                acc += ch.x ^ ch.y;
+            }
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
+__global__ void probe_soa(const uint32_t* __restrict__ hss, const uint32_t* __restrict__ ep,
+                          const uint32_t* __restrict__ args, uint32_t n, uint32_t na, const uint8_t* __restrict__ arity,
+                          uint32_t* __restrict__ sink) {
+    uint32_t acc = 0;
+    for (uint32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+        const uint32_t head = __ldcg(hss + y);
+        if (head == kDeadHead) continue;
+        const uint32_t ar = arity[head & kSymMask];
+        acc += __ldcg(ep + y);
+        for (uint32_t j = 0; j < na && j < 4; ++j)
+            if (j < ar) {
+                const uint32_t c = __ldcg(args + (size_t)j * n + y);
+                acc += __ldcg(hss + c) ^ __ldcg(ep + c);
+            }
+    }
+    if (acc == 0x9e3779b9u) sink[0] = acc;
+}
+
 __global__ void fill_random(uint32_t* idx, uint32_t n, uint64_t seed) {
     for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
         uint64_t z = seed + 0x9e3779b97f4a7c15ull * (k + 1);
@@ -296,6 +351,8 @@ struct trs_gpu_engine {
     uint32_t gb_cap = 0;
     int gb_blocks = 0;
     const void* jit_kernel = nullptr;  // the program's specialised step loop (jit.hpp), if compiled
+    const void* jit_kernel_ra = nullptr;  // ... its run-ahead build
+    bool use_ra = false;               // the pending run is in its run-ahead phase
     bool jit_off = false;              // this run uses the interpreted step loop
     double jit_seconds = 0;
     int jit_minb = 1;
@@ -328,7 +385,12 @@ struct trs_gpu_engine {
     uint32_t* d_stage = nullptr;          // trs_gpu_load H2D staging
     size_t stage_words = 0;
     uint32_t roots_out_cap = 0;
-    bool exported = false;                // staging holds the export of the current state
+    bool exported = false;                // staging holds the export of the current state (marked, renumbered)
+    bool packed = false;                  // ... and its columns are packed
+    std::vector<uint32_t> export_cta_live;  // live slots per renumbering range (rows of a range are contiguous)
+    uint32_t export_blocks = 0;
+    cudaStream_t stream2 = nullptr;       // D2H of packed column ranges, overlapping the next range's pack
+    cudaEvent_t pack_ev[8] = {};
     bool canon_ready = false;             // d_words holds the canonical words of that export
     uint32_t* d_canon = nullptr;          // canonical relabelling scratch (canon.cuh)
     size_t canon_words_cap = 0;
@@ -769,24 +831,30 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
 
 // Two register budgets per record width: MINB = 1 (no spills, 1 CTA of 512
 // threads per SM) and MINB = 2 (64 registers, 2 CTAs per SM, some spills).
-template <int W, int MINB>
+template <int W, int MINB, bool RA>
 const void* step_loop_ptr() {
-    return reinterpret_cast<const void*>(&step_loop<W, MINB>);
+    return reinterpret_cast<const void*>(&step_loop<W, MINB, RA>);
 }
 
-const void* step_loop_for(int W, int minb) {
+// The lean synchronous build (ra = false) or the run-ahead build.
+template <bool RA>
+const void* step_loop_for_ra(int W, int minb) {
     if (minb >= 2) {
         switch (W) {
-            case 8: return step_loop_ptr<8, 2>();
-            case 16: return step_loop_ptr<16, 2>();
-            default: return step_loop_ptr<32, 2>();
+            case 8: return step_loop_ptr<8, 2, RA>();
+            case 16: return step_loop_ptr<16, 2, RA>();
+            default: return step_loop_ptr<32, 2, RA>();
         }
     }
     switch (W) {
-        case 8: return step_loop_ptr<8, 1>();
-        case 16: return step_loop_ptr<16, 1>();
-        default: return step_loop_ptr<32, 1>();
+        case 8: return step_loop_ptr<8, 1, RA>();
+        case 16: return step_loop_ptr<16, 1, RA>();
+        default: return step_loop_ptr<32, 1, RA>();
     }
+}
+
+const void* step_loop_for(int W, int minb, bool ra) {
+    return ra ? step_loop_for_ra<true>(W, minb) : step_loop_for_ra<false>(W, minb);
 }
 
 // Dynamic shared memory of the step loop: program blob, the two single-CTA
@@ -823,8 +891,8 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
 // kernel when one was compiled (and not switched off for the run), else the
 // interpreted kernel of the record width.
 const void* loop_kernel(const trs_gpu_engine* e) {
-    if (e->jit_kernel && !e->jit_off) return e->jit_kernel;
-    return step_loop_for(e->W, e->minb);
+    if (e->jit_kernel && e->jit_kernel_ra && !e->jit_off) return e->use_ra ? e->jit_kernel_ra : e->jit_kernel;
+    return step_loop_for(e->W, e->minb, e->use_ra);
 }
 
 int grid_blocks(trs_gpu_engine* e, uint32_t blocks_per_sm) {
@@ -1213,6 +1281,9 @@ void trs_gpu_close(trs_gpu_engine* e) {
     cudaFree(e->d_nodes);
     if (e->load_a) cudaEventDestroy(e->load_a);
     if (e->load_b) cudaEventDestroy(e->load_b);
+    for (cudaEvent_t& ev : e->pack_ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->stream2) cudaStreamDestroy(e->stream2);
     cudaStreamDestroy(e->stream);
     delete e;
 }
@@ -1231,6 +1302,7 @@ int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
     // specialise the step loop for this program (jit.hpp); TRS_B200_JIT=0
     // keeps the interpreted kernel, and a failed compilation falls back to it
     e->jit_kernel = nullptr;
+    e->jit_kernel_ra = nullptr;
     e->jit_log.clear();
     e->jit_seconds = 0;
     const char* env = std::getenv("TRS_B200_JIT");
@@ -1243,16 +1315,20 @@ int trs_gpu_set_program(trs_gpu_engine* e, const trs_gpu_program* p) {
         JitResult jr = jit_compile(jit_source(e->blob.data(), e->W, e->max_vars), e->W, e->jit_minb);
         e->jit_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
         e->jit_kernel = jr.kernel;
+        e->jit_kernel_ra = jr.kernel_ra;
         e->jit_log = jr.log;
-        if (e->jit_kernel) {
+        if (e->jit_kernel && e->jit_kernel_ra) {
             // load the module now (lazy loading would otherwise happen at the
             // first launch, possibly behind a held stream gate)
             cudaFuncAttributes fa;
-            if (cudaFuncGetAttributes(&fa, e->jit_kernel) != cudaSuccess) {
+            if (cudaFuncGetAttributes(&fa, e->jit_kernel) != cudaSuccess ||
+                cudaFuncGetAttributes(&fa, e->jit_kernel_ra) != cudaSuccess) {
                 cudaGetLastError();
-                e->jit_kernel = nullptr;
+                e->jit_kernel = e->jit_kernel_ra = nullptr;
                 e->jit_log += "\nspecialised kernel failed to load";
             }
+        } else {
+            e->jit_kernel = e->jit_kernel_ra = nullptr;
         }
     }
     return TRS_GPU_OK;
@@ -1394,6 +1470,7 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     R = RunState{};
     if (opt_in) R.opt = *opt_in;
     e->minb = R.opt.variant == 2 ? 2 : 1;
+    e->use_ra = false;  // every run starts in the lean build
     e->jit_off = (R.opt.reserved[1] & 2u) != 0;
     // the resident arena costs L1 capacity on every grid sweep: reserve it
     // only for stores small enough to start resident (single-term runs)
@@ -1466,6 +1543,18 @@ int trs_gpu_run_wait(trs_gpu_engine* e, trs_gpu_stats* stats) {
             }
             if (!r) r = enqueue_launch(e);
             if (r) { result = r; break; }
+            continue;
+        }
+        if (c.status == kNeedRA) {
+            // a latency-bound phase began: continue in the run-ahead build
+            e->use_ra = true;
+            e->gb_blocks = 0;  // its occupancy may differ
+            R.blocks = grid_blocks(e, opt.blocks_per_sm);
+            if (opt.max_blocks && (int)opt.max_blocks < R.blocks) R.blocks = (int)opt.max_blocks;
+            if (int r = enqueue_launch(e)) {
+                result = r;
+                break;
+            }
             continue;
         }
         if (c.status == kValidate) {
@@ -1739,15 +1828,7 @@ ExportStaging export_staging(trs_gpu_engine* e, const Ctl& c) {
     return st;
 }
 
-// Mark from the roots, recount references, renumber and pack (export.cuh).
-int run_export(trs_gpu_engine* e, Ctl& c) {
-    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
-    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
-    const void* fn = e->W == 8 ? export_ptr<8>() : e->W == 16 ? export_ptr<16>() : export_ptr<32>();
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
-    const int blocks = std::min<int>(occ * e->sm_count, (int)kMaxGrid);
-    Params P = make_params(e, blocks);
+ExportArgs export_args(trs_gpu_engine* e, const Ctl& c) {
     ExportArgs X{};
     uint32_t* scratch = e->d_list[c.cur ^ 1];  // the frontier lives in list[c.cur]
     for (int k = 0; k < 3; ++k) X.queue[k] = scratch + (size_t)k * c.bump;
@@ -1761,6 +1842,20 @@ int run_export(trs_gpu_engine* e, Ctl& c) {
     X.nf = st.nf;
     X.roots_out = e->d_roots_out;
     X.ma = e->max_arity;
+    return X;
+}
+
+// Mark from the roots, recount references and renumber (export.cuh); the
+// columns are packed later, range by range (pack_export).
+int run_export(trs_gpu_engine* e, Ctl& c) {
+    CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    const void* fn = e->W == 8 ? export_ptr<8>() : e->W == 16 ? export_ptr<16>() : export_ptr<32>();
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, fn, kBlock, 0) != cudaSuccess || occ < 1) occ = 1;
+    const int blocks = std::min<int>(occ * e->sm_count, (int)kMaxGrid);
+    Params P = make_params(e, blocks);
+    ExportArgs X = export_args(e, c);
     uint32_t bump = c.bump;
     void* args[] = {&P, &X, &bump};
     CUDA_TRY(e, cudaMemsetAsync(X.counters, 0, sizeof(uint32_t) * 4, e->stream));
@@ -1768,8 +1863,12 @@ int run_export(trs_gpu_engine* e, Ctl& c) {
     reset_barrier(e);
     CUDA_TRY(e, cudaLaunchCooperativeKernel(fn, blocks, kBlock, args, 0, e->stream));
     uint32_t dangling = 0;
+    e->export_cta_live.assign(blocks, 0u);
+    e->export_blocks = (uint32_t)blocks;
     CUDA_TRY(e, cudaMemcpyAsync(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, e->stream));
     CUDA_TRY(e, cudaMemcpyAsync(&dangling, X.counters + 3, sizeof(uint32_t), cudaMemcpyDeviceToHost, e->stream));
+    CUDA_TRY(e, cudaMemcpyAsync(e->export_cta_live.data(), e->d_blocksum, sizeof(uint32_t) * blocks,
+                                cudaMemcpyDeviceToHost, e->stream));
     CUDA_TRY(e, cudaStreamSynchronize(e->stream));
     if (dangling) {
         e->exported = false;
@@ -1778,8 +1877,76 @@ int run_export(trs_gpu_engine* e, Ctl& c) {
                                             : "slot " + std::to_string(dangling) + " is not a live term");
     }
     e->exported = true;
+    e->packed = false;
     e->canon_ready = false;
     e->export_ctl = c;
+    return TRS_GPU_OK;
+}
+
+template <int W>
+void launch_pack(trs_gpu_engine* e, const ExportArgs& X, uint32_t n, const uint8_t* arity, uint32_t lo, uint32_t hi) {
+    const uint32_t A_idx = e->export_ctl.arena;
+    const int grid = std::max(1, std::min<int>(e->sm_count * 4, (int)(((hi - lo) / 8 + kBlock - 1) / kBlock)));
+    pack_range<W><<<grid, kBlock, 0, e->stream>>>(e->d_arena[A_idx], X, n, arity, lo, hi);
+}
+
+// Pack the exported columns, in up to 8 slot ranges; with host buffers, each
+// range's rows (contiguous: renumbering keeps arena order) are copied out on
+// a second stream while the next range packs.
+struct HostColumns {
+    uint32_t* hss;
+    uint32_t* args;
+    uint32_t* rcs;
+    uint8_t* nf;
+};
+
+int pack_export(trs_gpu_engine* e, const HostColumns* host) {
+    const Ctl& c = e->export_ctl;
+    const uint32_t n = c.export_n, bump = c.bump, ma = e->max_arity;
+    const ExportArgs X = export_args(e, c);
+    const uint8_t* arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
+    if (!e->stream2) CUDA_TRY(e, cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
+    const uint32_t B = std::max(1u, e->export_blocks);
+    const uint32_t span = bump > 1 ? bump - 1 : 0, chunk = (span + B - 1) / B;
+    const uint32_t G = std::min<uint32_t>(8, B);
+    uint32_t row = 1;  // row 0 is slot 0 (zeros, written by the export kernel)
+    for (uint32_t g = 0; g < G; ++g) {
+        const uint32_t b0 = g * B / G, b1 = (g + 1) * B / G;
+        const uint32_t lo = std::min<uint64_t>(bump, 1 + (uint64_t)b0 * chunk);
+        const uint32_t hi = std::min<uint64_t>(bump, 1 + (uint64_t)b1 * chunk);
+        uint32_t rows = 0;
+        for (uint32_t b = b0; b < b1; ++b) rows += e->export_cta_live[b];
+        if (hi > lo) {
+            switch (e->W) {
+                case 8: launch_pack<8>(e, X, n, arity, lo, hi); break;
+                case 16: launch_pack<16>(e, X, n, arity, lo, hi); break;
+                default: launch_pack<32>(e, X, n, arity, lo, hi); break;
+            }
+        }
+        if (host) {
+            if (!e->pack_ev[g]) CUDA_TRY(e, cudaEventCreateWithFlags(&e->pack_ev[g], cudaEventDisableTiming));
+            CUDA_TRY(e, cudaEventRecord(e->pack_ev[g], e->stream));
+            CUDA_TRY(e, cudaStreamWaitEvent(e->stream2, e->pack_ev[g], 0));
+            // this range's rows, plus row 0 with the first range
+            const uint32_t r0 = g == 0 ? 0 : row, r1 = row + rows;
+            if (r1 > r0) {
+                const size_t k = r1 - r0;
+                CUDA_TRY(e, cudaMemcpyAsync(host->hss + r0, X.hss + r0, 4 * k, cudaMemcpyDeviceToHost, e->stream2));
+                if (host->rcs)
+                    CUDA_TRY(e, cudaMemcpyAsync(host->rcs + r0, X.rcs + r0, 4 * k, cudaMemcpyDeviceToHost, e->stream2));
+                if (host->nf) CUDA_TRY(e, cudaMemcpyAsync(host->nf + r0, X.nf + r0, k, cudaMemcpyDeviceToHost, e->stream2));
+                if (host->args && ma)
+                    CUDA_TRY(e, cudaMemcpy2DAsync(host->args + r0, 4 * (size_t)n, X.args + r0, 4 * (size_t)n, 4 * k, ma,
+                                                  cudaMemcpyDeviceToHost, e->stream2));
+            }
+        }
+        row += rows;
+    }
+    if (row != n) return fail(e, TRS_GPU_CUDA, "export: renumbering ranges do not cover the exported rows");
+    if (host) CUDA_TRY(e, cudaStreamSynchronize(e->stream2));
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    CUDA_TRY(e, cudaGetLastError());
+    e->packed = true;
     return TRS_GPU_OK;
 }
 
@@ -1797,6 +1964,8 @@ int run_canon(trs_gpu_engine* e) {
         if (int r = run_export(e, c)) return r;
     }
     if (e->canon_ready) return TRS_GPU_OK;
+    if (!e->packed)
+        if (int r = pack_export(e, nullptr)) return r;
     const Ctl& c = e->export_ctl;
     const uint32_t n = c.export_n;
     const uint32_t ma = e->max_arity;
@@ -1906,6 +2075,16 @@ int trs_gpu_fetch_store(trs_gpu_engine* e, uint32_t* n, uint32_t* roots_out, uin
     *n = N;
     if (!hss) return TRS_GPU_OK;
     if (cap < N) return fail(e, TRS_GPU_INVALID, "fetch buffer too small");
+    if (!e->packed) {
+        // pack range by range, each range's rows copied out while the next packs
+        const HostColumns host{hss, args, refcounts, nf};
+        if (int r = pack_export(e, &host)) return r;
+        if (roots_out)
+            CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots_out, sizeof(uint32_t) * e->num_roots,
+                                        cudaMemcpyDeviceToHost, e->stream));
+        CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+        return TRS_GPU_OK;
+    }
     const ExportStaging st = export_staging(e, c);
     const uint32_t ma = e->max_arity;
     CUDA_TRY(e, cudaMemcpyAsync(hss, st.hss, sizeof(uint32_t) * N, cudaMemcpyDeviceToHost, e->stream));
@@ -1994,6 +2173,51 @@ int trs_gpu_canonical_all(trs_gpu_engine* e, uint32_t* words, uint64_t cap, uint
     if (root_nodes) CUDA_TRY(e, cudaMemcpy(root_nodes, e->d_nodes, sizeof(uint32_t) * R, cudaMemcpyDeviceToHost));
     if (words && cap >= e->canon_total)
         CUDA_TRY(e, cudaMemcpy(words, e->d_words, sizeof(uint32_t) * e->canon_total, cudaMemcpyDeviceToHost));
+    return TRS_GPU_OK;
+}
+
+int trs_gpu_layout_probe(trs_gpu_engine* e, uint32_t layout, uint32_t iters, double* ms_per_pass, uint64_t* nodes) {
+    if (!e || !e->loaded || !ms_per_pass || layout > 1) return TRS_GPU_INVALID;
+    REFUSE_PENDING(e);
+    cudaSetDevice(e->device);
+    if (int r = drain(e)) return r;
+    if (e->W != 8) return fail(e, TRS_GPU_INVALID, "layout probe: 8-word records only");
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    const uint32_t n = c.bump;
+    const uint32_t na = std::min<uint32_t>(e->max_arity, 4);
+    const uint32_t* A = e->d_arena[c.arena];
+    const uint8_t* arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
+    uint32_t* soa = nullptr;
+    uint32_t* sink = nullptr;
+    CUDA_TRY(e, cudaMalloc(&sink, 4));
+    if (layout == 1) {
+        CUDA_TRY(e, cudaMalloc(&soa, sizeof(uint32_t) * (size_t)n * (2 + na)));
+        to_soa<8><<<e->sm_count * 8, 256, 0, e->stream>>>(A, n, soa, soa + n, soa + 2 * (size_t)n, na);
+    }
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto pass = [&]() {
+        if (layout == 0)
+            probe_aos<8><<<e->sm_count * 8, 256, 0, e->stream>>>(A, n, arity, sink);
+        else
+            probe_soa<<<e->sm_count * 8, 256, 0, e->stream>>>(soa, soa + n, soa + 2 * (size_t)n, n, na, arity, sink);
+    };
+    pass();  // warm-up
+    cudaEventRecord(a, e->stream);
+    for (uint32_t k = 0; k < std::max(1u, iters); ++k) pass();
+    cudaEventRecord(b, e->stream);
+    cudaError_t err = cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(soa);
+    cudaFree(sink);
+    if (err != cudaSuccess) return fail(e, TRS_GPU_CUDA, std::string("layout probe: ") + cudaGetErrorString(err));
+    *ms_per_pass = ms / std::max(1u, iters);
+    if (nodes) *nodes = n;
     return TRS_GPU_OK;
 }
 

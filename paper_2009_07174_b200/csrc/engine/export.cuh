@@ -214,29 +214,8 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
     }
     grid_sync(P.ctl, nblocks, epoch);
     TRS_EXPORT_MARK(2)
-    // pack the columns: eight slots per thread per pass, their reference
-    // counts loaded together (most slots are garbage and only cost that load)
-    for (uint32_t y0 = 1 + tid * kPer; y0 < bump; y0 += nthreads * kPer) {
-        uint32_t rcs[kPer];
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) rcs[q] = y0 + q < bump ? __ldcg(X.newrc + y0 + q) : 0u;
-#pragma unroll
-        for (uint32_t q = 0; q < kPer; ++q) {
-        const uint32_t y = y0 + q;
-        const uint32_t rc = rcs[q];
-        if (!rc) continue;
-        const uint32_t k = __ldcg(X.map + y);
-        const uint32_t* R = A + (size_t)y * W;
-        const uint4 q0 = __ldcg(reinterpret_cast<const uint4*>(R));  // head, epoch, rc, waiter
-        const uint32_t sym = q0.x & kSymMask;
-        const uint32_t ar = arity[sym];
-        X.hss[k] = sym;
-        X.rcs[k] = rc;
-        X.nf[k] = epoch_nf(q0.y);
-        for (uint32_t j = 0; j < X.ma; ++j)
-            X.args[(size_t)j * n + k] = j < ar ? __ldcg(X.map + __ldcg(R + kWArgs + j)) : 0u;
-        }
-    }
+    // the columns are packed by pack_range, slot range by slot range, so the
+    // host can copy each range out while the next one packs
     if (tid == 0) {
         X.hss[0] = 0;
         X.rcs[0] = 0;
@@ -248,6 +227,38 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
     grid_sync(P.ctl, nblocks, epoch);
     TRS_EXPORT_MARK(3)
 #endif
+}
+
+// Pack live slots [lo, hi) of the arena into the reference columns: slot y
+// goes to row map[y]; rows of a slot range are contiguous (renumbering keeps
+// arena order).  Eight slots per thread per pass, their reference counts
+// loaded together (most slots are garbage and only cost that load).
+template <int W>
+__global__ void __launch_bounds__(kBlock) pack_range(const uint32_t* __restrict__ A, ExportArgs X, uint32_t n,
+                                                     const uint8_t* __restrict__ arity, uint32_t lo, uint32_t hi) {
+    constexpr uint32_t kPer = 8;
+    const uint32_t nthreads = gridDim.x * blockDim.x;
+    for (uint32_t y0 = lo + (blockIdx.x * blockDim.x + threadIdx.x) * kPer; y0 < hi; y0 += nthreads * kPer) {
+        uint32_t rcs[kPer];
+#pragma unroll
+        for (uint32_t q = 0; q < kPer; ++q) rcs[q] = y0 + q < hi ? __ldcg(X.newrc + y0 + q) : 0u;
+#pragma unroll
+        for (uint32_t q = 0; q < kPer; ++q) {
+            const uint32_t y = y0 + q;
+            const uint32_t rc = rcs[q];
+            if (!rc) continue;
+            const uint32_t k = __ldcg(X.map + y);
+            const uint32_t* R = A + (size_t)y * W;
+            const uint4 q0 = __ldcg(reinterpret_cast<const uint4*>(R));  // head, epoch, rc, waiter
+            const uint32_t sym = q0.x & kSymMask;
+            const uint32_t ar = arity[sym];
+            X.hss[k] = sym;
+            X.rcs[k] = rc;
+            X.nf[k] = epoch_nf(q0.y);
+            for (uint32_t j = 0; j < X.ma; ++j)
+                X.args[(size_t)j * n + k] = j < ar ? __ldcg(X.map + __ldcg(R + kWArgs + j)) : 0u;
+        }
+    }
 }
 
 }  // namespace trs_b200

@@ -208,7 +208,8 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
 }
 
 struct JitResult {
-    const void* kernel = nullptr;
+    const void* kernel = nullptr;     // step_loop<W, MINB, false>: the lean synchronous build
+    const void* kernel_ra = nullptr;  // step_loop<W, MINB, true>: the run-ahead build
     std::string log;
     double seconds = 0;
 };
@@ -216,12 +217,12 @@ struct JitResult {
 // Compile (or fetch from the process-wide cache) the specialised step loop.
 inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     static std::mutex mu;
-    static std::unordered_map<std::string, const void*> cache;
+    static std::unordered_map<std::string, std::pair<const void*, const void*>> cache;
     const std::string key = std::to_string(W) + "/" + std::to_string(minb) + (TRS_B200_PROFILE ? "p\n" : "\n") + src;
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
-        if (it != cache.end()) return JitResult{it->second, "", 0};
+        if (it != cache.end()) return JitResult{it->second.first, it->second.second, "", 0};
     }
     JitResult out;
     nvrtcProgram prog;
@@ -230,8 +231,10 @@ inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
         out.log = "nvrtcCreateProgram failed";
         return out;
     }
-    const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", " + std::to_string(minb) + ">";
+    const std::string name = "trs_b200::step_loop<" + std::to_string(W) + ", " + std::to_string(minb) + ", false>";
+    const std::string name_ra = "trs_b200::step_loop<" + std::to_string(W) + ", " + std::to_string(minb) + ", true>";
     nvrtcAddNameExpression(prog, name.c_str());
+    nvrtcAddNameExpression(prog, name_ra.c_str());
     // the specialisation is built like the library that loads it (profiling build or not)
     const char* verbose = std::getenv("TRS_B200_JIT_VERBOSE");  // ptxas register/spill report in the log
     const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
@@ -248,6 +251,9 @@ inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     const char* lowered = nullptr;
     nvrtcGetLoweredName(prog, name.c_str(), &lowered);
     const std::string lname = lowered ? lowered : "";
+    lowered = nullptr;
+    nvrtcGetLoweredName(prog, name_ra.c_str(), &lowered);
+    const std::string lname_ra = lowered ? lowered : "";
     size_t cb = 0;
     nvrtcGetCUBINSize(prog, &cb);
     std::vector<char> cubin(cb);
@@ -259,15 +265,17 @@ inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
         cudaGetLastError();
         return out;
     }
-    cudaKernel_t k = nullptr;
-    if (cudaLibraryGetKernel(&k, lib, lname.c_str()) != cudaSuccess) {
-        out.log += "\ncudaLibraryGetKernel failed for " + lname;
+    cudaKernel_t k = nullptr, kra = nullptr;
+    if (cudaLibraryGetKernel(&k, lib, lname.c_str()) != cudaSuccess ||
+        cudaLibraryGetKernel(&kra, lib, lname_ra.c_str()) != cudaSuccess) {
+        out.log += "\ncudaLibraryGetKernel failed for " + lname + " / " + lname_ra;
         cudaGetLastError();
         return out;
     }
     out.kernel = reinterpret_cast<const void*>(k);
+    out.kernel_ra = reinterpret_cast<const void*>(kra);
     std::lock_guard<std::mutex> g(mu);
-    cache[key] = out.kernel;
+    cache[key] = {out.kernel, out.kernel_ra};
     return out;
 }
 

@@ -165,7 +165,10 @@ constexpr uint32_t kEntHasPayload = 1;
 // except in the solo form (kSolo), which lane 0 runs alone for a one-entry
 // sweep.  Returns the warp's number of rewrites.
 
-template <int W, bool kRich, bool kSolo = false>
+// kRA: the run-ahead build of the step loop (continuations, publication
+// stamps, logical derive sweeps); without it logical and physical sweeps
+// coincide and the step is the lean synchronous one.
+template <int W, bool kRich, bool kRA, bool kSolo = false>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
                                               Slab& slab, bool valid, const uint32_t* entry, bool prof_req,
                                               PhaseClock& pc, bool may_cont, uint32_t& cont, uint32_t& tmax,
@@ -299,18 +302,19 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         // sweep_engine.cpp:80-81; with run-ahead: by another lane, whose
         // record writes need not be visible yet) -- is pending, and the slot
         // waits on the first such argument (:173-178).
-        T = (own_epoch & kTminBit) ? max(own_epoch & ~kTminBit, C.t0) : C.t0;
+        // (synchronous build: every derive of physical sweep s happens at
+        // logical sweep s, the reference's own schedule)
+        T = kRA ? ((own_epoch & kTminBit) ? max(own_epoch & ~kTminBit, C.t0) : C.t0) : s;
         bool pending = false;
 #pragma unroll
         for (int j = AE - 1; j >= 0; --j) {
             if ((uint32_t)j < ar) {
                 const uint32_t e = cep[j];
-                const bool ready = epoch_nf(e) && (C.ra ? (((e >> kEpochBits) & kStampMask) != C.stamp ||
+                const bool ready = epoch_nf(e) && (kRA ? (((e >> kEpochBits) & kStampMask) != C.stamp ||
                                                           a[j] == just_nf)
                                                        : (e & kEpochMask) < s);
-                if (ready) {
-                    T = max(T, (e & kEpochMask) + 1);
-                } else {
+                if (kRA && ready) T = max(T, (e & kEpochMask) + 1);
+                if (!ready) {
                     pending = true;
                     wpos = j;
                 }
@@ -513,7 +517,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             if (lane == 0) off = atomicAdd(C.claim_ctr, size);
             off = w_bcast<kSolo>(off, 0);
             // run-ahead feeds on the slots the sweep's worst case leaves over
-            slab.room = (uint64_t)off + size <= C.claim_soft ? 1u : 0u;
+            if (kRA) slab.room = (uint64_t)off + size <= C.claim_soft ? 1u : 0u;
             const uint64_t start = (uint64_t)C.bump + off;
             if (start + total > C.cap) {
                 // not even this step's slots fit: the reference raises
@@ -555,8 +559,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActNf) {
         uint32_t* R = rec<W>(arena, i);
         R[kWEpoch] = T | (C.stamp << kEpochBits);
-        tmax = max(tmax, T);
-        just_nf = i;
+        if (kRA) {
+            tmax = max(tmax, T);
+            just_nf = i;
+        }
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -596,8 +602,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             if ((uint32_t)j >= sar) b[j] = 0;
         uint32_t* R = rec<W>(arena, i);
         *reinterpret_cast<uint2*>(R) = make_uint2(shead, T | (C.stamp << kEpochBits));
-        tmax = max(tmax, T);
-        just_nf = i;
+        if (kRA) {
+            tmax = max(tmax, T);
+            just_nf = i;
+        }
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
@@ -703,8 +711,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // and its arguments' readiness is judged as above, so what it reads is
     // what the reference would read.  Every continued step is backed by
     // cont_cost reserved output entries (a refused reservation pushes).
-    bool want = may_cont && slab.room != 0u && (wake != 0u || (act == kActBuild && (push_mask != 0u || root_push)));
-    if (C.cont_room) {
+    bool want = kRA && may_cont && slab.room != 0u && (wake != 0u || (act == kActBuild && (push_mask != 0u || root_push)));
+    if (kRA && C.cont_room) {
         const uint32_t wm = kSolo ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
         if (wm) {
             uint32_t ok = 0;
@@ -722,7 +730,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         want = false;
     }
     cont = 0;
-    if (want) {
+    if (kRA && want) {
         if (wake) {
             cont = wake;
         } else if (root_push) {
@@ -834,7 +842,7 @@ __device__ __forceinline__ bool ra_more(const Params& P, const StepCtx& C, uint3
 // All warps of CTAs [block_rank, nblocks) process the frontier in q-entry
 // chunks (chunk_lanes); returns this thread's share of the rewrite count
 // (lane 0 of each warp holds its warp's count).
-template <int W, bool kRich>
+template <int W, bool kRich, bool kRA>
 __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const Prog& G, uint32_t* arena,
                                                           const StepCtx& C, const Frontier& F,
                                                           const uint32_t* __restrict__ in, uint32_t block_rank,
@@ -850,7 +858,7 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
             const uint32_t v = k * q + lane;
             const bool valid = lane < q && v < F.M;
             const uint32_t* entry = valid ? in + (size_t)frontier_phys(F, v) * W : in;
-            rw += warp_step<W, kRich>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc,
+            rw += warp_step<W, kRich, kRA>(P, G, arena, C, slab, valid, entry, prof && (TRS_B200_PROFILE || warp == 0), pc,
                                       false, cont, tmax, just_nf, pushes);
         }
         return lane == 0 ? rw : 0ull;
@@ -867,6 +875,20 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     uint32_t k = block_rank * kWarps + warp;
     uint32_t s0 = k * q < F.M ? slot_of(k) : 0u;
     uint32_t s1 = (k + gw) * q < F.M ? slot_of(k + gw) : 0u;
+    if (!kRA) {
+        // synchronous build: every lane of the warp steps through its entries together
+        for (; k * q < F.M; k += gw) {
+            const uint32_t s2 = (k + 2 * gw) * q < F.M ? slot_of(k + 2 * gw) : 0u;
+            if (s1) asm volatile("prefetch.L2 [%0];" ::"l"(rec<W>(arena, s1)));
+            uint32_t slot = s0;
+            rw += warp_step<W, kRich, kRA>(P, G, arena, C, slab, slot != 0u, &slot,
+                                           prof && (TRS_B200_PROFILE || warp == 0), pc, false, cont, tmax, just_nf,
+                                           pushes);
+            s0 = s1;
+            s1 = s2;
+        }
+        return lane == 0 ? rw : 0ull;
+    }
     uint32_t steps = 0;
     for (;;) {
         const bool own = lane < q && k * q + lane < F.M;
@@ -885,7 +907,7 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
             steps = 0;
             pushes = 0;
         }
-        rw += warp_step<W, kRich>(P, G, arena, C, slab, slot != 0u, &slot, prof && (TRS_B200_PROFILE || warp == 0),
+        rw += warp_step<W, kRich, kRA>(P, G, arena, C, slab, slot != 0u, &slot, prof && (TRS_B200_PROFILE || warp == 0),
                                   pc, ra_more(P, C, steps), cont, tmax, just_nf, pushes);
     }
     return lane == 0 ? rw : 0ull;
@@ -1117,15 +1139,22 @@ struct SmallState {
 // P.ra_kill entries (a latency-bound phase: fib, Ackermann, reverse,
 // mergesort) and off at a wider one: lanes that ran ahead reach a wide phase
 // out of step, and a warp of lanes on different rules diverges.
-__device__ __forceinline__ void ra_track(const Params& P, Local& L, uint32_t m) {
-    if (!P.runahead) return;
+// The lean (synchronous) build returns true instead: it hands the run over
+// to the run-ahead build (kNeedRA), which switches on at its first sweep.
+template <bool kRA>
+__device__ __forceinline__ bool ra_track(const Params& P, Local& L, uint32_t m) {
+    if (!P.runahead) return false;
     if (m > P.ra_kill) {
         L.ra_narrow = 0;
         L.ra_on = 0;
-    } else if (++L.ra_narrow >= P.ra_warm) {
-        L.ra_on = 1;
-        L.ra_used = 1;
+        return false;
     }
+    if (L.ra_narrow < P.ra_warm) ++L.ra_narrow;
+    if (L.ra_narrow < P.ra_warm) return false;
+    if (!kRA) return true;
+    L.ra_on = 1;
+    L.ra_used = 1;
+    return false;
 }
 
 // The step context of physical sweep s over m frontier entries, swept by
@@ -1248,7 +1277,7 @@ __device__ uint32_t local_gc(const Params& P, const Prog& G, Smem& sm, uint32_t*
 }
 
 // Warp 0 of CTA 0 runs sweeps alone while the frontier fits one warp.
-template <int W>
+template <int W, bool kRA>
 __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, SmallState& ss, Local& L,
                             bool& just_collected, Slab& slab, uint32_t* arena, uint64_t cap, uint32_t slab_size,
                             uint32_t& tmax) {
@@ -1274,8 +1303,8 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                     if (slab_size == 0 && (uint64_t)L.bump + P.max_new + 1 > cap) break;
                     if (plan(P, L, 1, just_collected, 1) != kPlanSweep) break;
                     just_collected = false;
+                    if (ra_track<kRA>(P, L, 1)) break;  // hand over to the run-ahead build
                     const uint32_t s = L.sweep + 1;
-                    ra_track(P, L, 1);
                     const long long cs = prof ? clock64() : 0;
                     ss.count[sc1 ^ 1] = 0;
                     ss.claim = 0;
@@ -1285,7 +1314,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                     uint32_t width = 0, cont = 0, steps = 0, just_nf = 0, pushes = 0;
                     uint32_t slot = slist[sc1 * kSmallCap];
                     for (;;) {
-                        width += warp_step<W, false, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                        width += warp_step<W, false, kRA, true>(P, G, arena, C, slab, true, &slot, prof, pc,
                                                            ra_more(P, C, steps), cont, tmax, just_nf, pushes);
                         if (!cont) break;
                         slot = cont;
@@ -1328,8 +1357,8 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         if (slab_size == 0 && (uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap) break;
         if (plan(P, L, m, just_collected, 1) != kPlanSweep) break;
         just_collected = false;
+        if (ra_track<kRA>(P, L, m)) break;
         const uint32_t s = L.sweep + 1;
-        ra_track(P, L, m);
         const long long cs = prof ? clock64() : 0;
         if (lane == 0) {
             ss.count[sc ^ 1] = 0;
@@ -1347,7 +1376,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                 uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
                 uint32_t slot = slist[sc * kSmallCap];
                 for (;;) {
-                    w1 += warp_step<W, false, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                    w1 += warp_step<W, false, kRA, true>(P, G, arena, C, slab, true, &slot, prof, pc,
                                                     ra_more(P, C, steps), cont, tmax, just_nf, pushes);
                     if (!cont) break;
                     slot = cont;
@@ -1362,7 +1391,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
             uint32_t slot = lane < m ? slist[sc * kSmallCap + lane] : 0u;
             for (;;) {
-                width += warp_step<W, false>(P, G, arena, C, slab, slot != 0u, &slot, prof, pc,
+                width += warp_step<W, false, kRA>(P, G, arena, C, slab, slot != 0u, &slot, prof, pc,
                                              ra_more(P, C, steps), cont, tmax, just_nf, pushes);
                 if (!__any_sync(0xffffffffu, cont != 0u)) break;
                 slot = cont;
@@ -1405,7 +1434,7 @@ __device__ __forceinline__ void zero_next_claims(const Params& P, uint32_t sweep
 }
 
 // CTA 0 runs sweeps out of shared memory while the frontier is small.
-template <int W>
+template <int W, bool kRA>
 __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bool& just_collected,
                           uint32_t* slist, SmallState& ss, const Frontier& F, Slab& slab, uint32_t& tmax) {
     Ctl* ctl = P.ctl;
@@ -1475,7 +1504,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         if (plan(P, L, m, just_collected, kWarps) != kPlanSweep) break;
         if (P.warp_mode && m <= 32) {
             if (warp == 0) {
-                warp_sweeps<W>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size, tmax);
+                warp_sweeps<W, kRA>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size, tmax);
                 if ((threadIdx.x & 31) == 0) ss.L = L;
             }
             __syncthreads();
@@ -1488,8 +1517,8 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
             continue;
         }
         just_collected = false;
+        if (ra_track<kRA>(P, L, m)) break;
         const uint32_t s = L.sweep + 1;
-        ra_track(P, L, m);
         const uint64_t t0 = threadIdx.x == 0 ? global_ns() : 0;
         const bool profc = kProfBuild && P.profile == 1 && threadIdx.x == 0;
         const long long cs = profc ? clock64() : 0;
@@ -1506,7 +1535,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         const StepCtx C = make_ctx(P, L, s, &ss.claim, slist + (sc ^ 1) * kSmallCap, &ss.count[sc ^ 1], &ss.flags, cap,
                                    slab_size, slist, m, kWarps, &ss.cont_room);
         PhaseClock pc;
-        unsigned long long rw = cta_entries<W, false>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
+        unsigned long long rw = cta_entries<W, false, kRA>(P, G, arena, C, Fs, slist + sc * kSmallCap, 0, 1, slab,
                                                       profc, pc, tmax);
         const unsigned long long width = block_sum64(rw, sm);
         L.bump = (uint32_t)min((uint64_t)L.bump + ss.claim, cap);
@@ -1550,7 +1579,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
     }
 }
 
-template <int W, int MINB>
+template <int W, int MINB, bool kRA>
 __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     extern __shared__ __align__(16) uint8_t smem_raw[];
     __shared__ Smem sm;
@@ -1579,6 +1608,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
     Slab slab{0, 0, 1u};
     uint32_t tmax = 0;  // latest nf epoch this thread published (the run's logical sweep count)
+    uint32_t lean_last = 0;
     Frontier F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
 
     bool gc_truncated = false;
@@ -1646,6 +1676,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         if (pl == kPlanFinish) {
             // the first sweep whose frontier is empty (sweep_engine.cpp:147)
             if (leader) record(P, s, 0, L, 0, 0, 0);
+            lean_last = L.sweep0 + L.sweep;  // lean build: the last sweep with an nf event
             L.sweep = s;
             exit_status = kDone;
             break;
@@ -1670,11 +1701,15 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             // ---- single-CTA mode: CTA 0 runs sweeps out of shared memory,
             // the rest of the grid parks in the barrier
             const uint32_t before = L.sweep;
-            if (blockIdx.x == 0) run_small<W>(P, G, sm, L, just_collected, slist, ss, F, slab, tmax);
+            if (blockIdx.x == 0) run_small<W, kRA>(P, G, sm, L, just_collected, slist, ss, F, slab, tmax);
             grid_sync(ctl, nblocks, epoch, /*park=*/blockIdx.x != 0);
             load_local(L, ctl);
             F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
+            if (!kRA && P.runahead && L.ra_narrow >= P.ra_warm) {
+                exit_status = kNeedRA;
+                break;
+            }
             if (F.flags & kFlagCapacity) {
                 exit_status = kCapacity;
                 break;
@@ -1703,7 +1738,10 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         const uint32_t slack = (P.runahead && !P.rich && P.list_cap > base_ext)
                                    ? (uint32_t)min((P.list_cap - base_ext) / nblocks, (uint64_t)kMaxSlack)
                                    : 0u;
-        ra_track(P, L, m);  // every CTA sees the same m
+        if (ra_track<kRA>(P, L, m)) {  // every CTA sees the same m
+            exit_status = kNeedRA;
+            break;
+        }
         if (threadIdx.x == 0) {
             s_push = 0;
             s_flags = 0;
@@ -1736,11 +1774,11 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
 #endif
         unsigned long long rw =
 #if TRS_B200_RICH_ENTRIES
-            P.rich ? cta_entries<W, true>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
+            P.rich ? cta_entries<W, true, kRA>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
                                           wprof, wpc, tmax)
                    :
 #endif
-                     cta_entries<W, false>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
+                     cta_entries<W, false, kRA>(P, G, P.arena[L.arena], C, F, P.list[L.cur], blockIdx.x, nblocks, slab,
                                            wprof, wpc, tmax);
 #if TRS_B200_PROFILE
         if ((threadIdx.x & 31) == 0) atomicMax(&ctl->gcprof[s & 1], (unsigned long long)(clock64() - wt0));
@@ -1803,8 +1841,11 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     abandon_slab<W>(P.arena[L.arena], slab);
     // the latest nf epoch of this launch; finish_run turns it into the
     // logical sweep count
-    const uint32_t wt = __reduce_max_sync(0xffffffffu, tmax);
-    if ((threadIdx.x & 31) == 0 && wt) atomicMax(&ctl->tmax, wt);
+    // (lean build: logical = physical, the last sweep with an nf event is the
+    // last swept one)
+    const uint32_t wt = kRA ? __reduce_max_sync(0xffffffffu, tmax)
+                            : (exit_status == kDone ? lean_last : L.sweep0 + L.sweep);
+    if ((threadIdx.x & 31) == 0 && wt && (kRA || threadIdx.x == 0)) atomicMax(&ctl->tmax, wt);
     if (leader) {
         store_local(L, ctl);
         ctl->status = exit_status;

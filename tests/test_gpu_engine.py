@@ -561,3 +561,27 @@ def test_widths_clean_after_a_stopped_run(engine, budget):
         api.normalize_texts(g["text"], engine=engine, options=api.make_options(step_budget=budget))
     res = api.normalize_texts(g["text"], engine=engine)
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+
+
+@pytest.mark.parametrize("name", ["reverse64", "ackermann23", "mergesort64_s1"])
+def test_runahead_engages_on_chains(engine, name):
+    """A latency-bound run (narrow frontiers) hands over from the lean
+    synchronous build to the run-ahead build: far fewer physical sweeps than
+    the reference's sweeps, and the reference's widths all the same."""
+    g = CASES[name]
+    res = api.normalize_texts(g["text"], engine=engine)
+    assert res.total_rewrites == g["rewrites"] and res.sweeps == g["sweeps"]
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+    # 64 narrow sweeps in the lean build, then few physical sweeps for the rest
+    assert len(engine.phys_trace()) < 64 + (g["sweeps"] - 64) // 2
+    assert res.stats["launches"] >= 2  # lean build, then the run-ahead build
+
+
+def test_wide_run_stays_in_step(engine):
+    """transform(6) widens quickly: it never runs ahead, one physical sweep per
+    reference sweep, one launch."""
+    g = CASES["transform6"]
+    res = api.normalize_texts(g["text"], engine=engine)
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    assert len(engine.phys_trace()) == g["sweeps"] and res.stats["launches"] == 1

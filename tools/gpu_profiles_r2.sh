@@ -17,3 +17,4 @@ timeout 600 ncu --set full --clock-control none --import-source on -k regex:cano
     -o gpurun_out/ncu_canon python tools/canon_target.py > gpurun_out/ncu_canon.log 2>&1; echo "ncu canon rc=$?"
 timeout 600 ncu --set full --clock-control none -k regex:gather_probe -s 1 -c 1 \
     -o gpurun_out/ncu_probe python tools/probe_target.py > gpurun_out/ncu_probe.log 2>&1; echo "ncu probe rc=$?"
+timeout 600 python tools/layout_ab.py > gpurun_out/layout_ab.log 2>&1; timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_read.sum,l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum,l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum --clock-control none -k regex:probe_ --csv --log-file gpurun_out/ncu_layout.csv python tools/layout_ab.py > gpurun_out/ncu_layout.log 2>&1; echo "layout rc=$?"
