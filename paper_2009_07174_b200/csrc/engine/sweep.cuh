@@ -49,7 +49,14 @@ struct Slab {
 template <int W, bool kSolo = false>
 __device__ __forceinline__ void abandon_slab(uint32_t* arena, Slab& slab) {
     const uint32_t lane = kSolo ? 0u : (threadIdx.x & 31);
-    for (uint32_t x = slab.cur + lane; x < slab.end; x += kSolo ? 1u : 32u) rec<W>(arena, x)[kWHead] = kDeadHead;
+    // the whole record: collections and copies read the first quad (and
+    // move whole records) of every slot below the bump pointer
+    for (uint32_t x = slab.cur + lane; x < slab.end; x += kSolo ? 1u : 32u) {
+        uint4* R = reinterpret_cast<uint4*>(rec<W>(arena, x));
+        R[0] = make_uint4(kDeadHead, 0u, 0u, 0u);
+#pragma unroll
+        for (int q = 1; q < W / 4; ++q) R[q] = make_uint4(0u, 0u, 0u, 0u);
+    }
     slab.cur = slab.end = 0;
 }
 

@@ -51,6 +51,12 @@ __device__ void validate_store_device(const Params& P, const Prog& G, uint32_t a
     uint32_t* prev = P.val + 2 * P.capacity;
     const uint32_t tid = block_rank * kBlock + threadIdx.x;
     const uint32_t nthreads = nblocks * kBlock;
+    if (!monotone) {
+        // a collection renumbered the slots (or the launch is new): no epoch
+        // recorded before it is comparable, above the new bump pointer either
+        for (uint64_t x = tid; x < P.capacity; x += nthreads) prev[x] = 0u;
+        grid_sync(P.ctl, nblocks, epoch);
+    }
     // phase 1: count references, mark the frontier, check the arguments
     for (uint32_t x = 1 + tid; x < bump; x += nthreads) {
         const uint32_t* R = A + (size_t)x * W;

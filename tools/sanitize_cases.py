@@ -26,6 +26,8 @@ def main():
     cases = json.load(open(os.path.join(ROOT, "tests", "golden", "small.json")))["cases"]
     names = ["unit_two_waiters", "unit_shared_fresh", "unit_dupvar", "transform3", "fib10", "mergesort10_s3",
              "treemergesort_2_3_s5", "ackermann22", "reverse8", "fibbatch16_s1"]
+    if len(sys.argv) > 3:
+        names = names[: int(sys.argv[3])]
     eng = api.Engine(0)
     bad = 0
     for mode in modes:
