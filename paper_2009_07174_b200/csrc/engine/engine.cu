@@ -1487,7 +1487,10 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
         // an explicit budget below the default (sweep_engine.hpp:32) asks for the
         // reference's abort point: no run-ahead then
         const bool budget = R.opt.step_budget != 0 && R.opt.step_budget < 1000000000ull;
-        R.runahead = !budget && !R.opt.fixed_capacity && !(R.opt.reserved[1] & 4u) && !(ra && ra[0] == '0');
+        // (8-word records only: the wide-record run-ahead build spills and
+        // measured slower than the synchronous one on the sort configs)
+        R.runahead = !budget && !R.opt.fixed_capacity && !(R.opt.reserved[1] & 4u) && !(ra && ra[0] == '0') &&
+                     (e->W == 8 || (ra && ra[0] == '1'));
     }
     // widths of the last run go; the histogram is all zeros again
     if (e->hist_used)

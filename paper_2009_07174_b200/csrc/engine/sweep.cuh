@@ -566,10 +566,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActNf) {
         uint32_t* R = rec<W>(arena, i);
         R[kWEpoch] = T | (C.stamp << kEpochBits);
-        if (kRA) {
-            tmax = max(tmax, T);
-            just_nf = i;
-        }
+        tmax = max(tmax, T);
+        if (kRA) just_nf = i;
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -609,10 +607,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             if ((uint32_t)j >= sar) b[j] = 0;
         uint32_t* R = rec<W>(arena, i);
         *reinterpret_cast<uint2*>(R) = make_uint2(shead, T | (C.stamp << kEpochBits));
-        if (kRA) {
-            tmax = max(tmax, T);
-            just_nf = i;
-        }
+        tmax = max(tmax, T);
+        if (kRA) just_nf = i;
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
@@ -693,6 +689,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     }
     uint32_t wake = 0;  // the parent this lane's nf publication woke
     if (wword) {
+        // run-ahead: the parent the nf publication will most likely wake is
+        // the waiter word as loaded; its record is fetched while the CAS
+        // confirms it (the next step of this lane's chain starts there)
+        if (kRA && act != kActWait && own_waiter != 0u && own_waiter != kWoken)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(rec<W>(arena, own_waiter)));
         uint32_t old = atomicCAS(wword, wcmp, wval);
         if (act == kActWait) {
             // lost the subscription race (another subscriber, or the child
@@ -1615,7 +1616,6 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     uint32_t epoch = 0;  // barriers passed in this launch (the host zeroes bar_arrive)
     Slab slab{0, 0, 1u};
     uint32_t tmax = 0;  // latest nf epoch this thread published (the run's logical sweep count)
-    uint32_t lean_last = 0;
     Frontier F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
 
     bool gc_truncated = false;
@@ -1683,7 +1683,6 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         if (pl == kPlanFinish) {
             // the first sweep whose frontier is empty (sweep_engine.cpp:147)
             if (leader) record(P, s, 0, L, 0, 0, 0);
-            lean_last = L.sweep0 + L.sweep;  // lean build: the last sweep with an nf event
             L.sweep = s;
             exit_status = kDone;
             break;
@@ -1848,11 +1847,8 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
     abandon_slab<W>(P.arena[L.arena], slab);
     // the latest nf epoch of this launch; finish_run turns it into the
     // logical sweep count
-    // (lean build: logical = physical, the last sweep with an nf event is the
-    // last swept one)
-    const uint32_t wt = kRA ? __reduce_max_sync(0xffffffffu, tmax)
-                            : (exit_status == kDone ? lean_last : L.sweep0 + L.sweep);
-    if ((threadIdx.x & 31) == 0 && wt && (kRA || threadIdx.x == 0)) atomicMax(&ctl->tmax, wt);
+    const uint32_t wt = __reduce_max_sync(0xffffffffu, tmax);
+    if ((threadIdx.x & 31) == 0 && wt) atomicMax(&ctl->tmax, wt);
     if (leader) {
         store_local(L, ctl);
         ctl->status = exit_status;
