@@ -823,12 +823,16 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         }
     }
     if (prof) pc.t[3] += clock64() - c3;
-    if (C.hwin) {
-        const bool win = rewrote && T - C.hbase < kHistWin;
-        hist_add<kSolo>(C.hwin + (T - C.hbase), win);
-        hist_add<kSolo>(C.hist + (T - C.t0), rewrote && !win);
-    } else {
-        hist_add<kSolo>(C.hist + (T - C.t0), rewrote);
+    // (the lean build adds each sweep's width once, at its end: all its
+    // rewrites happen at the sweep's own logical sweep)
+    if (kRA) {
+        if (C.hwin) {
+            const bool win = rewrote && T - C.hbase < kHistWin;
+            hist_add<kSolo>(C.hwin + (T - C.hbase), win);
+            hist_add<kSolo>(C.hist + (T - C.t0), rewrote && !win);
+        } else {
+            hist_add<kSolo>(C.hist + (T - C.t0), rewrote);
+        }
     }
     if (kSolo) return rewrote ? 1u : 0u;
     return __popc(__ballot_sync(0xffffffffu, rewrote));
@@ -978,7 +982,11 @@ enum Plan : uint32_t { kPlanSweep, kPlanGc, kPlanGrow, kPlanFinish, kPlanTrace }
 __device__ __forceinline__ uint32_t plan(const Params& P, const Local& L, uint32_t m, bool just_collected,
                                          uint32_t nwarps) {
     const uint32_t s = L.sweep + 1;
-    if (s > P.trace_cap) return kPlanTrace;
+    // the physical trace, and the width histogram entry of a synchronous
+    // sweep (logical = physical), must exist before the sweep starts: a sweep
+    // whose lanes deferred for want of an entry would shift every later
+    // sweep of the lean build
+    if (s > P.trace_cap || s > P.hist_cap) return kPlanTrace;
     if (m == 0) return kPlanFinish;
     // worst case: every frontier slot rewrites with the largest template,
     // plus what slab hand-offs can strand (ensure_headroom, sweep_engine.cpp:290-303)
@@ -1332,6 +1340,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                     L.peak_bump = max(L.peak_bump, L.bump);
                     L.total += width;
                     L.maxw = width > L.maxw ? width : L.maxw;
+                    if (!kRA && width) atomicAdd(P.hist + (s - 1), (unsigned long long)width);
                     L.sweep = s;
                     L.small_sweeps++;
                     ss.sc = sc1 ^ 1;
@@ -1416,6 +1425,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
         const uint64_t now = global_ns();
         if (lane == 0) {
             ss.sc = sc ^ 1;
+            if (!kRA && width) atomicAdd(P.hist + (s - 1), (unsigned long long)width);
             record(P, s, width, L, m, 2, now - t_prev);
             if (prof) {
                 for (int k = 0; k < 4; ++k) P.ctl->prof[k] += pc.t[k];
@@ -1554,6 +1564,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
         L.small_sweeps++;
         if (threadIdx.x == 0) {
             ss.sc = sc ^ 1;
+            if (!kRA && width) atomicAdd(P.hist + (s - 1), width);
             record(P, s, width, L, m, resident ? 3 : 1, global_ns() - t0);
             if (profc) {
                 for (int k = 0; k < 4; ++k) ctl->prof[k] += pc.t[k];
@@ -1688,6 +1699,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             break;
         }
         if (pl == kPlanTrace) {
+            if (leader && s > P.hist_cap) atomicMax(&ctl->hist_need, s + 1);
             exit_status = kNeedTrace;
             break;
         }
@@ -1795,7 +1807,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         if (leader) pc = wpc;
 #endif
         rw = block_sum64(rw, sm);  // ends synchronised: the width window is complete
-        if (threadIdx.x < kHistWin && s_hwin[threadIdx.x])
+        if (kRA && threadIdx.x < kHistWin && s_hwin[threadIdx.x])
             atomicAdd(P.hist + (C.hbase - C.t0 + threadIdx.x), (unsigned long long)s_hwin[threadIdx.x]);
         if (threadIdx.x == 0) {
             region_off(P, L.cur ^ 1)[blockIdx.x] = out_off;
@@ -1815,6 +1827,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
         L.maxw = width > L.maxw ? width : L.maxw;
         L.sweep = s;
         if (leader) {
+            if (!kRA && width) atomicAdd(P.hist + (s - 1), width);
             record(P, s, width, L, m, 0, global_ns() - t0);
 #if TRS_B200_PROFILE
             if (s <= P.trace_cap) P.trace[s - 1].free_len = (uint32_t)__ldcg(&ctl->gcprof[s & 1]);

@@ -588,3 +588,20 @@ def test_wide_run_stays_in_step(engine):
     res = api.normalize_texts(g["text"], engine=engine)
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
     assert len(engine.phys_trace()) == g["sweeps"] and res.stats["launches"] == 1
+
+
+@pytest.mark.parametrize("knobs", [{}, {"no_runahead": 1}])
+def test_histogram_growth_keeps_the_sweeps(knobs):
+    """A fresh engine starts with a 65,536-sweep width histogram and trace;
+    Ackermann(3,6) needs 344,976 sweeps, so both grow mid-run (the step loop
+    exits and is relaunched, in the synchronous and the run-ahead build), and
+    the sweep count and every width stay the reference's."""
+    fx = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "fullsize_ref.json")))["ackermann36"]
+    eng = api.Engine(0)
+    try:
+        res = api.normalize_texts(W.ackermann(3, 6), engine=eng, options=api.make_options(**knobs))
+        assert res.total_rewrites == fx["rewrites"] and res.sweeps == fx["sweeps"]
+        assert hashlib.sha1(res.widths.astype("<u8").tobytes()).hexdigest() == fx["widths_sha1"]
+        assert res.stats["launches"] >= 3
+    finally:
+        eng.close()
