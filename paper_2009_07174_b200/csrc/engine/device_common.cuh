@@ -285,6 +285,7 @@ struct Prog {
     const DPlan* plans;
     const uint16_t* mrow;
     const uint32_t* mtab;
+    const uint16_t* chain;  // null: no constant chains
     uint32_t npos;
     uint32_t max_new;
 };
@@ -302,6 +303,7 @@ __device__ __forceinline__ Prog view_prog(const uint8_t* blob) {
     p.mrow = reinterpret_cast<const uint16_t*>(blob + h->off_mrow);
     p.mtab = reinterpret_cast<const uint32_t*>(blob + h->off_mtab);
     p.npos = h->npos;
+    p.chain = h->chains ? reinterpret_cast<const uint16_t*>(blob + h->off_chain) : nullptr;
     p.max_new = h->max_new_slots;
     return p;
 }

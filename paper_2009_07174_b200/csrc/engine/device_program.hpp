@@ -141,6 +141,16 @@ struct DPlan {
 };
 static_assert(sizeof(DPlan) == 8, "DPlan layout");
 
+// Constant chains.  A constant f() whose first rule (an arity-0 left-hand
+// side always matches) rewrites it in place into another constant g(),
+// building nothing, takes its next rewrites without looking at anything
+// else: f -> g -> ... at consecutive logical sweeps.  chain[f] = g for such
+// a step, kChainNf when f has no rules (it becomes nf), kChainNone otherwise.
+// The run-ahead build takes a whole chain in registers (transform's leaves:
+// A() -> B() -> ... -> End(), 26 rewrites, generators.cpp:84-110).
+constexpr uint16_t kChainNone = 0xFFFF, kChainNf = 0xFFFE;
+constexpr uint32_t kChainMax = 4096;
+
 struct ProgHeader {
     uint32_t num_symbols;
     uint32_t num_rules;
@@ -159,6 +169,8 @@ struct ProgHeader {
     uint32_t off_mrow;        // uint16_t[num_symbols][npos]: match-table row per checked position, 0xFFFF none
     uint32_t off_mtab;        // uint32_t rows of num_symbols rule masks
     uint32_t npos;            // positions per symbol: rec_args(W) children + kPlanSlots slots (0: no tables)
+    uint32_t off_chain;       // uint16_t[num_symbols]: constant chains (kChain*), see below
+    uint32_t chains;          // the program has at least one constant-chain step
     uint32_t bytes;           // total blob size (multiple of 16)
 };
 

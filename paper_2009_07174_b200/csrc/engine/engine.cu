@@ -353,6 +353,7 @@ struct trs_gpu_engine {
     const void* jit_kernel = nullptr;  // the program's specialised step loop (jit.hpp), if compiled
     const void* jit_kernel_ra = nullptr;  // ... its run-ahead build
     bool use_ra = false;               // the pending run is in its run-ahead phase
+    bool has_chains = false;           // the program has constant chains (device_program.hpp)
     bool jit_off = false;              // this run uses the interpreted step loop
     double jit_seconds = 0;
     int jit_minb = 1;
@@ -797,6 +798,24 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     off = align16(off + 2 * (uint32_t)mrow.size());
     h.off_mtab = off;
     off = align16(off + 4 * (uint32_t)mtab.size());
+    // constant chains (device_program.hpp)
+    std::vector<uint16_t> chain(p->num_symbols, kChainNone);
+    for (uint32_t f = 0; f < p->num_symbols; ++f) {
+        if (p->arity[f] != 0) continue;
+        if (p->rule_begin[f] == p->rule_begin[f + 1]) {
+            chain[f] = kChainNf;
+            continue;
+        }
+        const trs_gpu_rule& R = p->rules[p->rule_begin[f]];
+        if (!(R.root_ref & TRS_GPU_REF_NODE) || R.num_instrs != 1) continue;
+        const uint32_t g = p->instrs[R.first_instr].symbol;
+        if (p->arity[g] == 0 && g < kChainNf) {
+            chain[f] = (uint16_t)g;
+            h.chains = 1;
+        }
+    }
+    h.off_chain = off;
+    off = align16(off + 2 * (uint32_t)chain.size());
     h.bytes = off;
     if (h.bytes > kMaxProgramBytes) return fail(e, TRS_GPU_INVALID, "program blob above 40 KiB");
     std::vector<uint8_t> blob(h.bytes, 0);
@@ -814,6 +833,7 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     std::memcpy(blob.data() + h.off_plans, plans.data(), sizeof(DPlan) * plans.size());
     if (!mrow.empty()) std::memcpy(blob.data() + h.off_mrow, mrow.data(), 2 * mrow.size());
     if (!mtab.empty()) std::memcpy(blob.data() + h.off_mtab, mtab.data(), 4 * mtab.size());
+    std::memcpy(blob.data() + h.off_chain, chain.data(), 2 * chain.size());
     e->blob = std::move(blob);
     e->max_arity = max_arity;
     e->max_new = max_new;
@@ -822,6 +842,7 @@ int build_blob(trs_gpu_engine* e, const trs_gpu_program* p) {
     if (dyn_base(e) > kSmemBudget)
         return fail(e, TRS_GPU_INVALID, "program + binding columns exceed the step loop's shared memory");
     e->num_symbols = p->num_symbols;
+    e->has_chains = reinterpret_cast<const ProgHeader*>(e->blob.data())->chains != 0;
     e->arity.assign(p->arity, p->arity + p->num_symbols);
     e->rule_source.resize(p->num_rules);
     for (uint32_t r = 0; r < p->num_rules; ++r) e->rule_source[r] = p->rules[r].source_order;
@@ -1470,18 +1491,11 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     R = RunState{};
     if (opt_in) R.opt = *opt_in;
     e->minb = R.opt.variant == 2 ? 2 : 1;
-    e->use_ra = false;  // every run starts in the lean build
+    e->use_ra = false;  // every run starts in the lean build (but see below)
     e->jit_off = (R.opt.reserved[1] & 2u) != 0;
     // the resident arena costs L1 capacity on every grid sweep: reserve it
     // only for stores small enough to start resident (single-term runs)
     e->resident_on = !(R.opt.reserved[1] & 1u) && resident_slots(e) != 0 && e->input_n <= resident_slots(e) / 2;
-    R.blocks = grid_blocks(e, R.opt.blocks_per_sm);
-    if (R.opt.max_blocks && (int)R.opt.max_blocks < R.blocks) R.blocks = (int)R.opt.max_blocks;
-    if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
-    if (!e->ev_a) CUDA_TRY(e, cudaEventCreate(&e->ev_a));
-    if (!e->ev_b) CUDA_TRY(e, cudaEventCreate(&e->ev_b));
-    R.a = e->ev_a;
-    R.b = e->ev_b;
     {
         const char* ra = std::getenv("TRS_B200_RUNAHEAD");
         // an explicit budget below the default (sweep_engine.hpp:32) asks for the
@@ -1490,8 +1504,19 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
         // (8-word records only: the wide-record run-ahead build spills and
         // measured slower than the synchronous one on the sort configs)
         R.runahead = !budget && !R.opt.fixed_capacity && !(R.opt.reserved[1] & 4u) && !(ra && ra[0] == '0') &&
-                     (e->W == 8 || (ra && ra[0] == '1'));
+                     R.opt.validate < 2 && (e->W == 8 || (ra && ra[0] == '1'));
     }
+    // a program with constant chains starts in the run-ahead build: it takes
+    // a chain in registers (transform's leaves) where the lean build would
+    // sweep it rewrite by rewrite
+    if (R.runahead && e->has_chains) e->use_ra = true;
+    R.blocks = grid_blocks(e, R.opt.blocks_per_sm);
+    if (R.opt.max_blocks && (int)R.opt.max_blocks < R.blocks) R.blocks = (int)R.opt.max_blocks;
+    if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
+    if (!e->ev_a) CUDA_TRY(e, cudaEventCreate(&e->ev_a));
+    if (!e->ev_b) CUDA_TRY(e, cudaEventCreate(&e->ev_b));
+    R.a = e->ev_a;
+    R.b = e->ev_b;
     // widths of the last run go; the histogram is all zeros again
     if (e->hist_used)
         CUDA_TRY(e, cudaMemsetAsync(e->d_hist, 0, sizeof(unsigned long long) * e->hist_used, e->stream));

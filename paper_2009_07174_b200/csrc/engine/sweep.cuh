@@ -38,7 +38,7 @@ __device__ __forceinline__ uint32_t* bind_base(const Params& P, uint32_t* slist)
     return slist + 2 * kSmallCap + threadIdx.x;
 }
 
-enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild, kActDefer };
+enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild, kActDefer, kActChain };
 
 struct Slab {
     uint32_t cur, end;  // warp-uniform: [cur, end) are this warp's unused fresh slots
@@ -199,6 +199,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     uint32_t act = kActNone;
     uint32_t i = 0, sym = 0, ar = 0, rule = 0, wchild = 0, wpos = 0, cursor = 0;
     uint32_t T = 0;  // logical sweep of this derive
+    uint32_t chain_k = 0, chain_f = 0;  // run-ahead: constant-chain rewrites taken in registers, final symbol
     uint32_t a[MAXA];
     // level-synchronous matcher state (DPlan): children's first argument
     // quads, grandchild slot heads, and the argument quads of two slots
@@ -333,6 +334,18 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         } else if (T - C.t0 >= C.hist_cap || T >= kEpochMask - 1) {
             // past the width histogram: the host grows it (kPlanTrace)
             act = kActDefer;
+        } else if (kRA && ar == 0 && G.chain && G.chain[sym] < kChainNf) {
+            // a constant chain: its rewrites happen at T, T + 1, ... whatever
+            // else happens (nothing is read), so they are taken here, in
+            // registers, and only the final state is written
+            uint32_t f = sym, k = 0;
+            while (k < kChainMax && G.chain[f] < kChainNf && T + k + 1 - C.t0 < C.hist_cap) {
+                f = G.chain[f];
+                ++k;
+            }
+            chain_k = k;
+            chain_f = f;
+            act = G.chain[f] == kChainNf ? kActNf : kActChain;
         } else if (pl.fast) {
             planned = true;
             // level 2: grandchild slots (nf below an nf child: stable)
@@ -565,12 +578,24 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         wval = i;
     } else if (act == kActNf) {
         uint32_t* R = rec<W>(arena, i);
-        R[kWEpoch] = T | (C.stamp << kEpochBits);
-        tmax = max(tmax, T);
+        if (kRA && chain_k) {
+            // the chain ends in a constant without rules: nf after its last rewrite
+            *reinterpret_cast<uint2*>(R) = make_uint2(chain_f, (T + chain_k) | (C.stamp << kEpochBits));
+            rewrote = true;
+        } else {
+            R[kWEpoch] = T | (C.stamp << kEpochBits);
+        }
+        tmax = max(tmax, T + chain_k);
         if (kRA) just_nf = i;
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
+    } else if (kRA && act == kActChain) {
+        // the chain stopped at a rule that builds or looks deeper (or at the
+        // histogram's end): the slot carries on from there at T + chain_k
+        *reinterpret_cast<uint2*>(rec<W>(arena, i)) = make_uint2(chain_f, kTminBit | (T + chain_k));
+        rewrote = true;
+        root_push = true;
     } else if (act == kActCollapse) {
         const DRule& Rl = G.rules[rule];
 #if TRS_GEN
@@ -719,7 +744,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // and its arguments' readiness is judged as above, so what it reads is
     // what the reference would read.  Every continued step is backed by
     // cont_cost reserved output entries (a refused reservation pushes).
-    bool want = kRA && may_cont && slab.room != 0u && (wake != 0u || (act == kActBuild && (push_mask != 0u || root_push)));
+    bool want = kRA && may_cont && slab.room != 0u &&
+                (wake != 0u || ((act == kActBuild || act == kActChain) && (push_mask != 0u || root_push)));
     if (kRA && C.cont_room) {
         const uint32_t wm = kSolo ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
         if (wm) {
@@ -753,6 +779,10 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         push1 = wake;
     }
     if (act == kActBuild) npush = __popc(push_mask) + (root_push ? 1u : 0u);
+    if (kRA && act == kActChain) {
+        npush = root_push ? 1u : 0u;
+        push1 = i;
+    }
     if (act == kActDefer) {
         npush = 1;
         push1 = i;
@@ -825,17 +855,25 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     if (prof) pc.t[3] += clock64() - c3;
     // (the lean build adds each sweep's width once, at its end: all its
     // rewrites happen at the sweep's own logical sweep)
+    // (a constant chain's k rewrites at T .. T + k - 1, one entry at a time:
+    // the lanes of a warp on the same chain add together)
+    uint32_t nrw = rewrote ? (chain_k ? chain_k : 1u) : 0u;
     if (kRA) {
-        if (C.hwin) {
-            const bool win = rewrote && T - C.hbase < kHistWin;
-            hist_add<kSolo>(C.hwin + (T - C.hbase), win);
-            hist_add<kSolo>(C.hist + (T - C.t0), rewrote && !win);
-        } else {
-            hist_add<kSolo>(C.hist + (T - C.t0), rewrote);
+        const uint32_t steps = kSolo ? nrw : __reduce_max_sync(0xffffffffu, nrw);
+        for (uint32_t j = 0; j < steps; ++j) {
+            const bool on = j < nrw;
+            const uint32_t Tj = T + j;
+            if (C.hwin) {
+                const bool win = on && Tj - C.hbase < kHistWin;
+                hist_add<kSolo>(C.hwin + (Tj - C.hbase), win);
+                hist_add<kSolo>(C.hist + (Tj - C.t0), on && !win);
+            } else {
+                hist_add<kSolo>(C.hist + (Tj - C.t0), on);
+            }
         }
     }
-    if (kSolo) return rewrote ? 1u : 0u;
-    return __popc(__ballot_sync(0xffffffffu, rewrote));
+    if (kSolo) return nrw;
+    return kRA ? __reduce_add_sync(0xffffffffu, nrw) : __popc(__ballot_sync(0xffffffffu, rewrote));
 }
 
 // Run-ahead output entries per CTA per grid sweep, at most.

@@ -55,6 +55,14 @@ UNIT = {
     # a shared fresh node built twice by one template (structural RHS sharing)
     "unit_shared_fresh": "sort T = A() | B() | F(T) | G(T, T) | H(T);\nvar X : T;\n"
                          "eqn F(X) = G(H(X), H(X));\n    H(A()) = B();\ninput F(F(A()));\n",
+    # constant chains (A() -> B() -> C(), no rules on C) under a parent that
+    # matches the chain's end, and a chain that stops at a building rule
+    "unit_chain_nf": "sort T = A() | B() | C() | D() | F(T) | G(T, T);\nvar X : T;\n"
+                     "eqn A() = B();\n    B() = C();\n    F(C()) = G(A(), D());\n    D() = A();\n"
+                     "input G(F(A()), F(B()));\n",
+    "unit_chain_into_build": "sort T = A() | B() | C() | F(T) | H(T, T);\nvar X : T;\n"
+                             "eqn A() = B();\n    B() = F(C());\n    F(X) = H(X, X);\n"
+                             "input H(A(), F(A()));\n",
     # a polled parent: two parents waiting on one shared non-nf node
     "unit_two_waiters": "sort T = A() | B() | F(T) | G(T, T) | K(T, T) | H(T);\nvar X : T; Y : T;\n"
                         "eqn F(X) = K(G(H(X), H(X)), H(X));\n    H(A()) = B();\n    G(X, Y) = Y;\n"
