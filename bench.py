@@ -536,7 +536,8 @@ def main():
             e2e_host.append([round(1e3 * (b - a), 3) for a, b in ((th0, th1), (th1, th2), (th2, th3), (th3, th4))])
             e2e_ms.append(e0.elapsed_time(e1))
             d2h_bytes.append(N * (4 + 4 * ma + 4 + 1) + 4 * len(roots))
-            launches_e2e = 3 + 3 * s_run["launches"] + 1  # load (3), prep + loop + finish per launch, export
+            # load (3); prep + step loop + finish per launch; export; pack, in 8 slot ranges
+            launches_e2e = 3 + 3 * s_run["launches"] + 1 + 8
     e2e_clocks.__exit__(None, None, None)
     e2e_max = reduce(sum(e2e_ms), torch.distributed.ReduceOp.MAX if world > 1 else None)
     e2e_value = all_rw / (e2e_max * 1e-3)

@@ -581,13 +581,19 @@ def test_runahead_engages_on_chains(engine, name, monkeypatch):
     assert res.stats["launches"] >= 2  # lean build, then the run-ahead build
 
 
-def test_wide_run_stays_in_step(engine):
-    """transform(6) widens quickly: it never runs ahead, one physical sweep per
-    reference sweep, one launch."""
-    g = CASES["transform6"]
+@pytest.mark.parametrize("name", ["transform6", "unit_chain_nf", "unit_chain_into_build"])
+def test_constant_chains_in_registers(engine, name):
+    """A program with constant chains (A() -> B() -> ...: transform's leaves)
+    starts in the run-ahead build, which takes each chain in registers: the
+    widths stay the reference's while the physical sweeps drop."""
+    g = CASES[name]
     res = api.normalize_texts(g["text"], engine=engine)
+    assert res.total_rewrites == g["rewrites"] and res.sweeps == g["sweeps"]
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
-    assert len(engine.phys_trace()) == g["sweeps"] and res.stats["launches"] == 1
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+    assert res.stats["launches"] == 1  # the run-ahead build from the start
+    if name == "transform6":
+        assert len(engine.phys_trace()) < g["sweeps"]
 
 
 @pytest.mark.parametrize("knobs", [{}, {"no_runahead": 1}])
