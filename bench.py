@@ -423,15 +423,13 @@ def main():
     jit = eng.jit_info()
     stream = torch.cuda.ExternalStream(eng.stream, device=dev)
 
-    # device-resident inputs (value path) and pinned host inputs (e2e path)
+    # device-resident inputs (value path); the e2e path reads the host store
+    # itself, which the front end flattened straight into page-locked memory
+    # (host/trs_host.hpp PinnedAlloc)
     d_hss = torch.from_numpy(v["hss"].view(np.int32)).to(dev)
     d_args = torch.from_numpy(v["args"].view(np.int32)).to(dev)
     d_rc = torch.from_numpy(v["refcounts"].view(np.int32)).to(dev)
     roots = v["roots"].copy()
-    p_hss = torch.from_numpy(v["hss"].view(np.int32)).pin_memory()
-    p_args = torch.from_numpy(v["args"].view(np.int32)).pin_memory()
-    p_rc = torch.from_numpy(v["refcounts"].view(np.int32)).pin_memory()
-    p_roots = torch.from_numpy(roots.view(np.int32)).pin_memory()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     torch.cuda.synchronize()
 
@@ -490,7 +488,7 @@ def main():
     # (trs_gpu_fetch_store: device export + D2H of hss, args, refcounts, nf, roots)
     import ctypes
 
-    h2d = (p_hss.numel() + p_args.numel() + p_rc.numel() + p_roots.numel()) * 4
+    h2d = (v["hss"].size + v["args"].size + v["refcounts"].size + v["roots"].size) * 4
     d2h_bytes, e2e_ms, e2e_host = [], [], []
     out = None
     ma = int(v["maxarity"])
@@ -507,8 +505,8 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         th0 = time.perf_counter()
-        rc = L.trs_gpu_load(eng._h, v["n"], p_roots.data_ptr(), len(roots), p_hss.data_ptr(),
-                            p_args.data_ptr(), v["maxarity"], p_rc.data_ptr(), 0)
+        rc = L.trs_gpu_load(eng._h, v["n"], v["roots_ptr"], v["num_roots"], v["hss_ptr"], v["args_ptr"],
+                            v["maxarity"], v["rc_ptr"], 0)
         assert rc == 0, eng._err()
         th1 = time.perf_counter()
         s_run = eng.run()
@@ -609,9 +607,11 @@ def main():
         "cpu_baseline": cpu,
         "e2e": {"value": e2e_value, "unit": "rewrites/s", "h2d_bytes_per_step": h2d,
                 "d2h_bytes_per_step": int(statistics.mean(d2h_bytes)),
-                "path": "trs_gpu_load (pinned host SoA) + trs_gpu_run + trs_gpu_fetch_store (device export: "
-                        "mark from the roots, recount references, renumber, pack; D2H of the reference TermStore "
-                        "columns into pinned host memory), CUDA events on the engine stream",
+                "path": "trs_gpu_load (the host SoA store, flattened by the front end straight into page-locked "
+                        "memory) + trs_gpu_run + trs_gpu_fetch_store (device export: mark from the roots, recount "
+                        "references, renumber; pack in slot ranges, each range's D2H of the reference TermStore "
+                        "columns into pinned host memory overlapping the next range's pack), CUDA events on the "
+                        "engine stream",
                 "ms_per_step": statistics.mean(e2e_ms), "gpu_launches_per_step": launches_e2e,
                 "step_ms": [round(x, 3) for x in e2e_ms], "clocks": e2e_clocks.summary(),
                 "host_ms_load_run_export_fetch": e2e_host[-1] if e2e_host else None,

@@ -718,7 +718,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         // the waiter word as loaded; its record is fetched while the CAS
         // confirms it (the next step of this lane's chain starts there)
         if (kRA && act != kActWait && own_waiter != 0u && own_waiter != kWoken)
-            asm volatile("prefetch.global.L1 [%0];" ::"l"(rec<W>(arena, own_waiter)));
+            asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, own_waiter)));  // generic: no-op on the resident arena
         uint32_t old = atomicCAS(wword, wcmp, wval);
         if (act == kActWait) {
             // lost the subscription race (another subscriber, or the child

@@ -2,9 +2,12 @@
 // const SweepOptions&) (proj/include/trs/sweep_engine.hpp:47) on the B200
 // engine behind trs_gpu.h, plus the extern "C" surface the Python mirror,
 // the tests and bench.py bind with ctypes.
+#include <cuda_runtime.h>
+
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <new>
 #include <memory>
 #include <mutex>
 
@@ -49,6 +52,32 @@ trs_gpu_engine* engine_for(int device) {
 }
 
 }  // namespace
+
+// Page-locked allocations carry a 16-byte tag so that frees know which
+// allocator they came from (cudaHostAlloc, or malloc without a device).
+void* pinned_alloc(std::size_t bytes) {
+    constexpr std::size_t kTag = 16;
+    void* p = nullptr;
+    const bool have_device = trs_gpu_device_count() > 0;
+    if (have_device && cudaHostAlloc(&p, bytes + kTag, cudaHostAllocDefault) == cudaSuccess) {
+        *static_cast<std::uint32_t*>(p) = 0x50494e4eu;  // "PINN"
+    } else {
+        if (have_device) cudaGetLastError();
+        p = std::malloc(bytes + kTag);
+        if (!p) throw std::bad_alloc();
+        *static_cast<std::uint32_t*>(p) = 0x48454150u;  // "HEAP"
+    }
+    return static_cast<char*>(p) + kTag;
+}
+
+void pinned_free(void* q) noexcept {
+    if (!q) return;
+    void* p = static_cast<char*>(q) - 16;
+    if (*static_cast<std::uint32_t*>(p) == 0x50494e4eu)
+        cudaFreeHost(p);
+    else
+        std::free(p);
+}
 
 // Load, run and write the normal form back into `store` with the given engine.
 SweepTrace run_with(trs_gpu_engine* e, TermStore& store, const FlatProgram& flat, const gpu::GpuOptions& o) {

@@ -208,6 +208,29 @@ FlatProgram flatten(const RewriteSystem& system, const DispatchTable& table);
 
 // ---- term store (proj/include/trs/term_store.hpp) ---------------------------
 
+// Page-locked host memory for the store's columns (cudaHostAlloc), so load
+// flattens the input straight into memory the device copies from without a
+// staging copy (trs_gpu_load's H2D is then a direct DMA); plain heap memory
+// where no CUDA device is present.  Defined in gpu_run.cpp.
+void* pinned_alloc(std::size_t bytes);
+void pinned_free(void* p) noexcept;
+
+template <class T>
+struct PinnedAlloc {
+    using value_type = T;
+    PinnedAlloc() = default;
+    template <class U>
+    PinnedAlloc(const PinnedAlloc<U>&) noexcept {}
+    T* allocate(std::size_t n) { return static_cast<T*>(pinned_alloc(n * sizeof(T))); }
+    void deallocate(T* p, std::size_t) noexcept { pinned_free(p); }
+    template <class U>
+    bool operator==(const PinnedAlloc<U>&) const noexcept { return true; }
+    template <class U>
+    bool operator!=(const PinnedAlloc<U>&) const noexcept { return false; }
+};
+template <class T>
+using pinned_vector = std::vector<T, PinnedAlloc<T>>;
+
 // Host mirror of the reference TermStore layout: slot 0 is never a term,
 // args column-major (args[j * n + i]), refcounts include one pin per root.
 struct TermStore {
@@ -216,10 +239,10 @@ struct TermStore {
     std::uint32_t maxarity = 0;
     std::vector<std::uint32_t> roots;
     std::vector<std::uint32_t> arity_of;
-    std::vector<std::uint32_t> hss;
-    std::vector<std::uint32_t> args;
-    std::vector<std::uint32_t> refcounts;
-    std::vector<std::uint8_t> nf;
+    pinned_vector<std::uint32_t> hss;
+    pinned_vector<std::uint32_t> args;
+    pinned_vector<std::uint32_t> refcounts;
+    pinned_vector<std::uint8_t> nf;
 
     std::uint32_t root() const { return roots.empty() ? 0 : roots[0]; }
     std::uint32_t arg(std::uint32_t j, std::uint32_t i) const { return args[static_cast<std::size_t>(j) * n + i]; }
