@@ -33,7 +33,7 @@ def main():
     tag = sys.argv[2] if len(sys.argv) > 2 else "r1"
     out = [f"# {tag} ncu summaries (specialised step loop): ncu --set full --clock-control none --import-source on",
            "# one steady-state launch each; captured with tools/gpu_profiles*.sh, summarised by tools/ncu_summary.py",
-           "#   step_loop: python tools/profile_target.py <workload>   (-k regex:step_loop -s 1 -c 1)",
+           "#   step_loop: python tools/profile_target.py <workload>   (--profile-from-start off -k regex:step_loop: every launch of the 2nd run)",
            "#   export_store: python tools/e2e_parts.py                (-k regex:export_store -c 1)",
            "# ncu times are replayed/serialised: compare shares, not absolutes", ""]
     traffic = {}
@@ -48,19 +48,29 @@ def main():
         rows = list(csv.reader(r.splitlines()))
         if len(rows) < 3:
             continue
-        h, u, v = rows[0], rows[1], rows[2]
-        out.append(f"## {c}: {desc}  ({v[h.index('Kernel Name')]})")
-        for w in WANT:
-            i = h.index(w)
-            out.append(f"{w:80s} {v[i]:>22s} {u[i]}")
-        rd = float(v[h.index('dram__bytes_read.sum')]) * SCALE[u[h.index('dram__bytes_read.sum')]]
-        wr = float(v[h.index('dram__bytes_write.sum')]) * SCALE[u[h.index('dram__bytes_write.sum')]]
-        out.append(f"{'dram bytes per launch (read+write)':80s} {rd + wr:22.4e} byte")
+        h, u = rows[0], rows[1]
+        launches = [v for v in rows[2:] if len(v) == len(h)]
+        names = ", ".join(v[h.index('Kernel Name')] for v in launches)
+        out.append(f"## {c}: {desc}  ({len(launches)} launch(es) of one run: {names})")
+        total = 0.0
+        for n, v in enumerate(launches):
+            if len(launches) > 1:
+                out.append(f"# launch {n}: {v[h.index('Kernel Name')]}")
+            for w in WANT:
+                i = h.index(w)
+                out.append(f"{w:80s} {v[i]:>22s} {u[i]}")
+            rd = float(v[h.index('dram__bytes_read.sum')]) * SCALE[u[h.index('dram__bytes_read.sum')]]
+            wr = float(v[h.index('dram__bytes_write.sum')]) * SCALE[u[h.index('dram__bytes_write.sum')]]
+            out.append(f"{'dram bytes of this launch (read+write)':80s} {rd + wr:22.4e} byte")
+            total += rd + wr
+        out.append(f"{'dram bytes per run (all launches, read+write)':80s} {total:22.4e} byte")
         out.append("")
-        traffic[key] = rd + wr
-    with open(os.path.join(ROOT, "profiles", f"{tag}_ncu_summary.txt"), "w") as f:
+        traffic[key] = total
+    dest = sys.argv[3] if len(sys.argv) > 3 else os.path.join(ROOT, "profiles")
+    os.makedirs(dest, exist_ok=True)
+    with open(os.path.join(dest, f"{tag}_ncu_summary.txt"), "w") as f:
         f.write("\n".join(out))
-    with open(os.path.join(ROOT, "profiles", "traffic.json"), "w") as f:
+    with open(os.path.join(dest, "traffic.json"), "w") as f:
         json.dump(traffic, f, indent=1)
     print("\n".join(out))
 

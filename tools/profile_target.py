@@ -1,9 +1,11 @@
 """Profiling target: one warm run, then the profiled run of the same batch.
 
-    ncu -k regex:step_loop -s 1 -c 1 ... python tools/profile_target.py fibbatch
+    ncu --profile-from-start off -k regex:step_loop ... python tools/profile_target.py fibbatch
 
-The arena is pre-sized so each run is exactly one step-loop launch (no
-growth relaunch), so `-s 1 -c 1` captures the second, steady-state run.
+The arena is pre-sized so no run regrows it; only the second, steady-state
+run is inside the profiler range (cudaProfilerStart/Stop), so ncu captures
+every step-loop launch of that run: the lean build and, when the run hands
+over to run-ahead (kNeedRA), the run-ahead build.
 """
 import json
 import os
@@ -21,8 +23,16 @@ systems = [api.System(t) for t in texts_for(name)]
 store = api.Store.load(systems)
 eng = api.Engine(0)
 eng.set_program(systems[0])
+import torch  # noqa: E402
+
 for rep in range(2):
     eng.load(store, capacity=capacity)
+    if rep == 1:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.start()
     st = eng.run()
+    if rep == 1:
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     print(json.dumps({"rep": rep, "kernel_ms": st["kernel_ms"], "launches": st["launches"], "regrows": st["regrows"],
                       "sweeps": st["sweeps"], "rewrites": st["total_rewrites"]}), flush=True)
