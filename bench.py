@@ -253,13 +253,21 @@ def gather_curve(device, api):
     return out
 
 
+def engine_accesses(c: dict) -> int:
+    """Random accesses per SURVEY.md 8(d) that this engine's step loop makes:
+    the model's A without its refcount RMWs (the step loop keeps no
+    refcounts; the collectors recount them, gc.cuh recount_refs)."""
+    return int(c["A"]) - int(c["counts"]["rc_rmw"])
+
+
 def per_config_table(eng, api, W, counts, fullsize, hbm_peak, gather_gbps, cpu_sweep):
     """Single-GPU timing + bit-exact parity of every BASELINE config (one
     warm-up, best of two timed runs), with the reference's CPU engines timed
     on this host: seq (1 core, every config) and sweep (nproc workers; the
     configs it finishes in seconds unless --cpu-sweep).  Rooflines:
     `gather_frac` is the SURVEY 8(d) model (4 B x A against the measured
-    uniformly random 4-B gather); it can exceed 1 where accesses hit L2, so
+    uniformly random 4-B gather, A without the refcount RMWs the step loop
+    skips); it can exceed 1 where accesses hit L2, so
     `dram_frac` (ncu DRAM bytes of the same launch, profiles/traffic.json,
     over the run time against the measured HBM copy bandwidth) and the
     sector efficiency (4 A + S_min) / DRAM bytes sit beside it."""
@@ -316,7 +324,7 @@ def per_config_table(eng, api, W, counts, fullsize, hbm_peak, gather_gbps, cpu_s
                 row["parity"]["widths"] = fx[0]["widths_sha1"] == hashlib.sha1(widths.tobytes()).hexdigest()
             row["parity"]["source"] = "tests/golden/fullsize_ref.json (unmodified reference, make_fullsize.py)"
         if all(cs):
-            a = sum(c["A"] for c in cs)
+            a = sum(engine_accesses(c) for c in cs)
             smin = sum(c["S_min"] for c in cs)
             row["gather_gbps"] = 4 * a / t / 1e9
             row["gather_frac"] = row["gather_gbps"] / gather_gbps if gather_gbps else None
@@ -569,7 +577,8 @@ def main():
     cs = [counts.get(f"{key}_s{s}") for s in seeds]
     roofline = None
     if all(cs):
-        A = sum(c["A"] for c in cs)
+        A = sum(engine_accesses(c) for c in cs)
+        A_survey = sum(c["A"] for c in cs)
         smin = sum(c["S_min"] for c in cs)
         t = kernel_ms * 1e-3
         alg_bytes = 32 * A + smin
@@ -580,7 +589,10 @@ def main():
             "kernel": "step_loop<8> (persistent cooperative sweep loop)",
             "algorithmic_bytes_per_launch": alg_bytes,
             "byte_model": "32 B x A (one DRAM sector per random access) + S_min (frontier streaming), "
-                          "SURVEY.md 8(d); A, S_min from the C oracle (tests/golden/workload_counts.json)",
+                          "SURVEY.md 8(d); A, S_min from the C oracle (tests/golden/workload_counts.json); A = the "
+                          "survey's random accesses minus the refcount RMWs this step loop does not make (refcounts "
+                          "are recounted by the collectors, gc.cuh recount_refs)",
+            "accesses": A, "accesses_survey_model": A_survey,
             "peak_kind": peak_kind,
             "sector_efficiency": (4 * A + smin) / traffic if traffic else None,
             "gather": {"achieved_gbps": 4 * A / t / 1e9, "roofline_gbps": gather_gbps,

@@ -272,7 +272,8 @@ int trs_gpu_dump_program(trs_gpu_engine* engine, const char* const* symbol_names
  * epoch word and arguments, then each argument's head and epoch word) over
  * every slot of the current store, read from the engine's 8-word AoS records
  * (layout 0) or from SoA columns built from them, the reference TermStore
- * layout (layout 1).  Reports ms per pass (CUDA events, `iters` passes) and
+ * layout (layout 1); layouts 2 and 3 are the same two visiting the slots in
+ * a hashed (random) order instead of slot order.  Reports ms per pass (CUDA events, `iters` passes) and
  * the slots scanned; ncu on trs_gpu_layout_probe's kernels gives the DRAM
  * bytes and sectors of each layout. */
 int trs_gpu_layout_probe(trs_gpu_engine* engine, uint32_t layout, uint32_t iters, double* ms_per_pass,
@@ -280,7 +281,9 @@ int trs_gpu_layout_probe(trs_gpu_engine* engine, uint32_t layout, uint32_t iters
 
 /* Exact count of slots with refcount > 0 in the current store: the
  * reference's live_terms (sweep_engine.cpp:122-123), which includes
- * garbage not yet collected. */
+ * garbage not yet collected.  Runs without validate keep no refcounts step
+ * by step; they are recounted from the store first (references from
+ * uncollected slots + root pins, the reference's ghost invariant). */
 int trs_gpu_live_count(trs_gpu_engine* engine, uint64_t* live);
 
 /* Raw store copy-back (reference TermStore layout): after a compacting pass
@@ -316,7 +319,8 @@ int trs_gpu_compact(trs_gpu_engine* engine, uint32_t max_rounds, trs_gpu_stats* 
 
 /* Raw copy of the device arena [0, n) into dst (record_words u32 per slot:
  * head|cursor<<24, nf epoch, refcount, waiter, args...) and of the root
- * slots into roots_out (may be NULL).  Two-call protocol on cap_bytes. */
+ * slots into roots_out (may be NULL).  Two-call protocol on cap_bytes.
+ * Refcount words are recounted first when the last run kept none. */
 int trs_gpu_fetch_records(trs_gpu_engine* engine, void* dst, uint64_t cap_bytes, uint64_t* bytes,
                           uint32_t* record_words, uint32_t* roots_out);
 

@@ -560,7 +560,8 @@ class Engine:
         return out
 
     def layout_probe(self, layout: int, iters: int = 5) -> dict:
-        """AoS (0) vs SoA (1) probe pass over the current store (trs_gpu_layout_probe)."""
+        """AoS (0) vs SoA (1) probe pass over the current store, in slot order or (+2) a hashed order
+        (trs_gpu_layout_probe)."""
         ms = ctypes.c_double(0)
         n = ctypes.c_uint64(0)
         _raise(lib().trs_gpu_layout_probe(self._h, layout, iters, ctypes.byref(ms), ctypes.byref(n)), self._err())

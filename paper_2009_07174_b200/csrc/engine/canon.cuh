@@ -249,4 +249,26 @@ __global__ void count_live(const uint32_t* __restrict__ A, uint32_t bump, unsign
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
 }
 
+// Host-launched refcount recount (gc.cuh recount_refs as two kernels), for
+// a store left by runs that kept no refcounts: before live_count, and before
+// a validating run continues such a store.
+template <int W>
+__global__ void recount_clear(uint32_t* __restrict__ A, uint32_t bump) {
+    for (uint32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < bump; y += gridDim.x * blockDim.x)
+        A[(size_t)y * W + kWRc] = 0u;
+}
+template <int W>
+__global__ void recount_add(uint32_t* __restrict__ A, uint32_t bump, const uint8_t* __restrict__ arity,
+                            const uint32_t* __restrict__ roots, uint32_t num_roots) {
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x, nthreads = gridDim.x * blockDim.x;
+    for (uint32_t y = 1 + tid; y < bump; y += nthreads) {
+        const uint32_t* R = A + (size_t)y * W;
+        const uint32_t head = R[kWHead];
+        if (head == kDeadHead) continue;
+        const uint32_t ar = arity[head & kSymMask];
+        for (uint32_t j = 0; j < ar; ++j) atomicAdd(A + (size_t)R[kWArgs + j] * W + kWRc, 1u);
+    }
+    for (uint32_t r = tid; r < num_roots; r += nthreads) atomicAdd(A + (size_t)roots[r] * W + kWRc, 1u);
+}
+
 }  // namespace trs_b200

@@ -134,6 +134,7 @@ struct Params {
     uint64_t list_cap;      // entries per frontier list buffer
     uint32_t validate;      // 2: quiescent-point scans before every grid sweep (validate.cuh)
     uint32_t* val;          // their scratch, 3 words per slot
+    uint32_t track_rc;      // steps keep refcounts (validate modes); otherwise collectors recount (gc.cuh)
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

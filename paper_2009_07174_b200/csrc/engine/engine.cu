@@ -262,11 +262,20 @@ __global__ void to_soa(const uint32_t* __restrict__ A, uint32_t n, uint32_t* __r
     }
 }
 
+// The probes visit every slot either in slot order or in a hashed order
+// (every parent a random slot, as a sweep's frontier order is at worst).
+__device__ __forceinline__ uint32_t probe_slot(uint32_t k, uint32_t n) {
+    uint64_t z = 0x9e3779b97f4a7c15ull * k;
+    z = (z ^ (z >> 31)) * 0xbf58476d1ce4e5b9ull;
+    return 1u + (uint32_t)((z ^ (z >> 29)) % (uint64_t)(n - 1));
+}
+
 template <int W>
 __global__ void probe_aos(const uint32_t* __restrict__ A, uint32_t n, const uint8_t* __restrict__ arity,
-                          uint32_t* __restrict__ sink) {
+                          uint32_t* __restrict__ sink, bool random_order) {
     uint32_t acc = 0;
-    for (uint32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+    for (uint32_t k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t y = random_order ? probe_slot(k, n) : k;
         const uint4 h = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)y * W));
         if (h.x == kDeadHead) continue;
         const uint4 a = __ldcg(reinterpret_cast<const uint4*>(A + (size_t)y * W + kWArgs));
@@ -285,9 +294,10 @@ __global__ void probe_aos(const uint32_t* __restrict__ A, uint32_t n, const uint
 
 __global__ void probe_soa(const uint32_t* __restrict__ hss, const uint32_t* __restrict__ ep,
                           const uint32_t* __restrict__ args, uint32_t n, uint32_t na, const uint8_t* __restrict__ arity,
-                          uint32_t* __restrict__ sink) {
+                          uint32_t* __restrict__ sink, bool random_order) {
     uint32_t acc = 0;
-    for (uint32_t y = 1 + blockIdx.x * blockDim.x + threadIdx.x; y < n; y += gridDim.x * blockDim.x) {
+    for (uint32_t k = 1 + blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+        const uint32_t y = random_order ? probe_slot(k, n) : k;
         const uint32_t head = __ldcg(hss + y);
         if (head == kDeadHead) continue;
         const uint32_t ar = arity[head & kSymMask];
@@ -354,6 +364,7 @@ struct trs_gpu_engine {
     const void* jit_kernel_ra = nullptr;  // ... its run-ahead build
     bool use_ra = false;               // the pending run is in its run-ahead phase
     bool has_chains = false;           // the program has constant chains (device_program.hpp)
+    bool rc_stale = false;             // a run without refcount tracking: live_count recounts first
     bool jit_off = false;              // this run uses the interpreted step loop
     double jit_seconds = 0;
     int jit_minb = 1;
@@ -1178,6 +1189,7 @@ int load_impl(trs_gpu_engine* e, uint32_t n, const uint32_t* roots, uint32_t num
     e->input_n = n;
     e->loaded = true;
     e->exported = false;
+    e->rc_stale = false;
     e->last_sweeps = 0;
     return TRS_GPU_OK;
 }
@@ -1199,6 +1211,36 @@ int fetch_arena(trs_gpu_engine* e, HostArena& h, std::vector<uint32_t>& roots) {
     CUDA_TRY(e, cudaMemcpy(h.words.data(), e->d_arena[c.arena], sizeof(uint32_t) * h.words.size(), cudaMemcpyDeviceToHost));
     roots.resize(e->num_roots);
     CUDA_TRY(e, cudaMemcpy(roots.data(), e->d_roots, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost));
+    return TRS_GPU_OK;
+}
+
+// Refcounts of a store that runs without tracking left stale (e->rc_stale):
+// recounted from the store (gc.cuh recount_refs), synchronously.
+int ensure_refcounts(trs_gpu_engine* e) {
+    if (!e->rc_stale) return TRS_GPU_OK;
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    Ctl c;
+    CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
+    uint32_t* A = e->d_arena[c.arena];
+    const uint8_t* arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
+    const int blocks = e->sm_count * 8;
+    switch (e->W) {
+        case 8:
+            recount_clear<8><<<blocks, 256, 0, e->stream>>>(A, c.bump);
+            recount_add<8><<<blocks, 256, 0, e->stream>>>(A, c.bump, arity, e->d_roots, e->num_roots);
+            break;
+        case 16:
+            recount_clear<16><<<blocks, 256, 0, e->stream>>>(A, c.bump);
+            recount_add<16><<<blocks, 256, 0, e->stream>>>(A, c.bump, arity, e->d_roots, e->num_roots);
+            break;
+        default:
+            recount_clear<32><<<blocks, 256, 0, e->stream>>>(A, c.bump);
+            recount_add<32><<<blocks, 256, 0, e->stream>>>(A, c.bump, arity, e->d_roots, e->num_roots);
+            break;
+    }
+    CUDA_TRY(e, cudaGetLastError());
+    CUDA_TRY(e, cudaStreamSynchronize(e->stream));
+    e->rc_stale = false;
     return TRS_GPU_OK;
 }
 
@@ -1450,13 +1492,21 @@ int enqueue_launch(trs_gpu_engine* e) {
     }
     {
         const char* rm = std::getenv("TRS_B200_RA_MAX");  // tuning hook
-        P.ra_max = rm ? (uint32_t)std::strtoul(rm, nullptr, 10) : (uint32_t)R.blocks * kWarps * 4u;
+        // defaults from tools/ra_sweep.py (profiles/r2_ra_sweep*.log): run-ahead in
+        // sweeps of up to one entry per lane, handed over after 64 sweeps of at
+        // most two per lane, 32 continued steps per lane and physical sweep
+        P.ra_max = rm ? (uint32_t)std::strtoul(rm, nullptr, 10) : (uint32_t)R.blocks * kWarps * 32u;
         const char* rk = std::getenv("TRS_B200_RA_KILL");
-        P.ra_kill = rk ? (uint32_t)std::strtoul(rk, nullptr, 10) : (uint32_t)R.blocks * kWarps * 8u;
+        P.ra_kill = rk ? (uint32_t)std::strtoul(rk, nullptr, 10) : (uint32_t)R.blocks * kWarps * 64u;
         const char* rw = std::getenv("TRS_B200_RA_WARM");
         P.ra_warm = rw ? (uint32_t)std::strtoul(rw, nullptr, 10) : 64u;
         const char* rs = std::getenv("TRS_B200_RA_STEPS");
-        P.ra_steps = rs ? (uint32_t)std::strtoul(rs, nullptr, 10) : 8u;
+        P.ra_steps = rs ? (uint32_t)std::strtoul(rs, nullptr, 10) : 32u;
+        // refcounts are kept step by step only for the validate modes (their
+        // checks read them); otherwise collectors and live_count recount
+        const char* tr = std::getenv("TRS_B200_TRACK_RC");  // A/B hook (tools/rc_ab.py)
+        P.track_rc = (opt.validate || (tr && tr[0] == '1')) ? 1u : 0u;
+        if (!P.track_rc) e->rc_stale = true;
     }
     void* args[] = {&P};
     cudaEventRecord(R.a, e->stream);
@@ -1510,6 +1560,9 @@ int trs_gpu_run_async(trs_gpu_engine* e, const trs_gpu_options* opt_in) {
     // a chain in registers (transform's leaves) where the lean build would
     // sweep it rewrite by rewrite
     if (R.runahead && e->has_chains) e->use_ra = true;
+    // a validating run checks refcounts: a store an untracked run left gets them recounted
+    if (R.opt.validate)
+        if (int r = ensure_refcounts(e)) return r;
     R.blocks = grid_blocks(e, R.opt.blocks_per_sm);
     if (R.opt.max_blocks && (int)R.opt.max_blocks < R.blocks) R.blocks = (int)R.opt.max_blocks;
     if (!e->h_ctl) CUDA_TRY(e, cudaMallocHost(&e->h_ctl, sizeof(Ctl)));
@@ -1767,6 +1820,7 @@ int trs_gpu_fetch_records(trs_gpu_engine* e, void* dst, uint64_t cap_bytes, uint
     if (bytes) *bytes = need;
     if (record_words) *record_words = (uint32_t)e->W;
     if (!dst || cap_bytes < need) return TRS_GPU_OK;
+    if (int r = ensure_refcounts(e)) return r;  // the records' refcount words as the reference keeps them
     CUDA_TRY(e, cudaMemcpyAsync(dst, e->d_arena[c.arena], need, cudaMemcpyDeviceToHost, e->stream));
     if (roots_out)
         CUDA_TRY(e, cudaMemcpyAsync(roots_out, e->d_roots, sizeof(uint32_t) * e->num_roots, cudaMemcpyDeviceToHost, e->stream));
@@ -2205,7 +2259,7 @@ int trs_gpu_canonical_all(trs_gpu_engine* e, uint32_t* words, uint64_t cap, uint
 }
 
 int trs_gpu_layout_probe(trs_gpu_engine* e, uint32_t layout, uint32_t iters, double* ms_per_pass, uint64_t* nodes) {
-    if (!e || !e->loaded || !ms_per_pass || layout > 1) return TRS_GPU_INVALID;
+    if (!e || !e->loaded || !ms_per_pass || layout > 3) return TRS_GPU_INVALID;
     REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
@@ -2219,7 +2273,8 @@ int trs_gpu_layout_probe(trs_gpu_engine* e, uint32_t layout, uint32_t iters, dou
     uint32_t* soa = nullptr;
     uint32_t* sink = nullptr;
     CUDA_TRY(e, cudaMalloc(&sink, 4));
-    if (layout == 1) {
+    const bool soa_layout = layout & 1u, random_order = layout & 2u;
+    if (soa_layout) {
         CUDA_TRY(e, cudaMalloc(&soa, sizeof(uint32_t) * (size_t)n * (2 + na)));
         to_soa<8><<<e->sm_count * 8, 256, 0, e->stream>>>(A, n, soa, soa + n, soa + 2 * (size_t)n, na);
     }
@@ -2227,10 +2282,11 @@ int trs_gpu_layout_probe(trs_gpu_engine* e, uint32_t layout, uint32_t iters, dou
     cudaEventCreate(&a);
     cudaEventCreate(&b);
     auto pass = [&]() {
-        if (layout == 0)
-            probe_aos<8><<<e->sm_count * 8, 256, 0, e->stream>>>(A, n, arity, sink);
+        if (!soa_layout)
+            probe_aos<8><<<e->sm_count * 8, 256, 0, e->stream>>>(A, n, arity, sink, random_order);
         else
-            probe_soa<<<e->sm_count * 8, 256, 0, e->stream>>>(soa, soa + n, soa + 2 * (size_t)n, n, na, arity, sink);
+            probe_soa<<<e->sm_count * 8, 256, 0, e->stream>>>(soa, soa + n, soa + 2 * (size_t)n, n, na, arity, sink,
+                                                              random_order);
     };
     pass();  // warm-up
     cudaEventRecord(a, e->stream);
@@ -2254,6 +2310,7 @@ int trs_gpu_live_count(trs_gpu_engine* e, uint64_t* live) {
     REFUSE_PENDING(e);
     cudaSetDevice(e->device);
     if (int r = drain(e)) return r;
+    if (int r = ensure_refcounts(e)) return r;
     Ctl c;
     CUDA_TRY(e, cudaMemcpy(&c, e->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost));
     unsigned long long* d = reinterpret_cast<unsigned long long*>(e->d_blocksum + kMaxGrid);  // scratch words

@@ -35,6 +35,30 @@ __device__ __forceinline__ uint32_t frontier_phys(const Frontier& f, uint32_t v)
     return f.off[lo] + (v - f.pref[lo]);
 }
 
+// Refcounts recounted from the store: rc(y) = references from uncollected
+// slots + root pins, the reference's ghost invariant (sweep_engine.cpp:335-359)
+// and so exactly what maintaining them rewrite by rewrite would leave.  The
+// step loop keeps no refcounts unless Params::track_rc (validate modes): no
+// derive reads them (garbage is always nf, so the frontier
+// needs no liveness test), and the argument updates were a fifth of the
+// batched configs' step-loop time (tools/rc_ab.py).  The collectors recount
+// first.  Threads [tid, nthreads) of the caller's group; `sync` is its barrier.
+template <int W, typename Sync>
+__device__ __forceinline__ void recount_refs(const Params& P, const Prog& G, uint32_t* A, uint32_t bump, uint32_t tid,
+                                             uint32_t nthreads, Sync sync) {
+    for (uint32_t x = 1 + tid; x < bump; x += nthreads) rec<W>(A, x)[kWRc] = 0u;
+    sync();
+    for (uint32_t x = 1 + tid; x < bump; x += nthreads) {
+        const uint32_t* R = rec<W>(A, x);
+        const uint32_t head = R[kWHead];
+        if (head == kDeadHead) continue;
+        const uint32_t ar = G.arity[head & kSymMask];
+        for (uint32_t j = 0; j < ar; ++j) atomicAdd(rec<W>(A, R[kWArgs + j]) + kWRc, 1u);
+    }
+    for (uint32_t r = tid; r < P.num_roots; r += nthreads) atomicAdd(rec<W>(A, __ldcg(P.roots + r)) + kWRc, 1u);
+    sync();
+}
+
 // Returns the new bump pointer.  The caller has staged `in` (regions of
 // list buffer `cur`) and abandoned every warp's slab; on return the
 // frontier is one dense region of buffer cur ^ 1 and arena_idx is flipped.
@@ -60,6 +84,7 @@ __device__ uint32_t gc_compact(const Params& P, Smem& sm, const Prog& G, uint32_
 #else
 #define TRS_GC_MARK(k)
 #endif
+    if (!P.track_rc) recount_refs<W>(P, G, A, bump, tid, nthreads, [&]() { grid_sync(P.ctl, nblocks, epoch); });
     // phase 1: claim refcount-zero slots and drop their argument references.
     // A thread follows the cascade it triggers for at most max_hops claimed
     // slots (64 inside the step loop, bounding the pause; unbounded for the

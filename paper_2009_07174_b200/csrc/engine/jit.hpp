@@ -178,7 +178,7 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
             }
             // every reuse of a bound variable adds one reference (sweep_engine.cpp:251-253)
             for (uint32_t v : var_refs)
-                body += "            rc_upd<S>(rec<W>(arena, gb[" + std::to_string(v) + "]) + kWRc, 1);\n";
+                body += "            if (rc) rc_upd<S>(rec<W>(arena, gb[" + std::to_string(v) + "]) + kWRc, 1);\n";
             build += "        case " + std::to_string(r) + ": {\n" + body + "            break;\n        }\n";
         }
     }
@@ -202,7 +202,8 @@ inline std::string jit_source(const uint8_t* blob, int W, uint32_t max_vars) {
            "    switch (rule) {\n" +
            csrc + "        default: return 0u;\n    }\n}\n";
     src += "template <int W, bool S>\n__device__ __forceinline__ void gen_build(uint32_t rule, uint32_t* arena, uint32_t fresh,\n"
-           "    uint32_t i, uint32_t ar, const uint32_t (&gb)[TRS_GEN_MAXV], uint32_t tnext) {\n    switch (rule) {\n" +
+           "    uint32_t i, uint32_t ar, const uint32_t (&gb)[TRS_GEN_MAXV], uint32_t tnext, bool rc) {\n"
+           "    switch (rule) {\n" +
            build + "        default: break;\n    }\n}\n}  // namespace trs_b200\n#include \"sweep.cuh\"\n";
     return src;
 }

@@ -534,7 +534,13 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             abandon_slab<W, kSolo>(arena, slab);
             const uint32_t size = max(C.slab, total);
             uint32_t off = 0;
-            if (lane == 0) off = atomicAdd(C.claim_ctr, size);
+            if (kSolo) {
+                // the solo step runs alone on the device: plain counters
+                off = *C.claim_ctr;
+                *C.claim_ctr = off + size;
+            } else if (lane == 0) {
+                off = atomicAdd(C.claim_ctr, size);
+            }
             off = w_bcast<kSolo>(off, 0);
             // run-ahead feeds on the slots the sweep's worst case leaves over
             if (kRA) slab.room = (uint64_t)off + size <= C.claim_soft ? 1u : 0u;
@@ -638,7 +644,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
             if ((uint32_t)j >= sar) break;
-            rc_update(rec<W>(arena, b[j]) + kWRc, 1);
+            if (P.track_rc) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
         }
         wword = R + kWWaiter;
         wcmp = own_waiter;
@@ -647,7 +653,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
 #if TRS_GEN
-        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb, kTminBit | (T + 1));
+        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb, kTminBit | (T + 1), P.track_rc != 0);
 #else
         const uint32_t nfresh = Rl.new_slots;
         for (uint32_t k = 0; k <= nfresh; ++k) {
@@ -691,7 +697,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
             for (int j = 0; j < AE; ++j) {
                 if ((vmask >> j) == 0u) break;
-                if ((vmask >> j) & 1u) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
+                if (((vmask >> j) & 1u) && P.track_rc) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
             }
         }
 #endif
@@ -705,7 +711,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     }
     // the rewritten root drops its old children (after the additions, as
     // the reference orders them; sweep_engine.cpp:255-256)
-    if (rewrote) {
+    if (rewrote && P.track_rc) {
 #pragma unroll
         for (int j = 0; j < AE; ++j) {
             if ((uint32_t)j >= ar) break;
@@ -719,7 +725,16 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         // confirms it (the next step of this lane's chain starts there)
         if (kRA && act != kActWait && own_waiter != 0u && own_waiter != kWoken)
             asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, own_waiter)));  // generic: no-op on the resident arena
-        uint32_t old = atomicCAS(wword, wcmp, wval);
+        uint32_t old;
+        if (kSolo) {
+            // nothing else runs: the subscription and the publication are a
+            // read and a write (an nf publication's word is the one loaded
+            // with the record, unchanged since: only subscribers write it)
+            old = act == kActWait ? *wword : wcmp;
+            if (old == wcmp) *wword = wval;
+        } else {
+            old = atomicCAS(wword, wcmp, wval);
+        }
         if (act == kActWait) {
             // lost the subscription race (another subscriber, or the child
             // turned nf this very sweep): poll next sweep
@@ -750,7 +765,13 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         const uint32_t wm = kSolo ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
         if (wm) {
             uint32_t ok = 0;
-            if (lane == 0) {
+            if (kSolo) {
+                const int need = (int)C.cont_cost;
+                if (*C.cont_room >= need) {
+                    *C.cont_room -= need;
+                    ok = 1;
+                }
+            } else if (lane == 0) {
                 const int need = __popc(wm) * (int)C.cont_cost;
                 const int before = atomicSub(C.cont_room, need);
                 if (before >= need)
@@ -796,7 +817,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     const uint32_t ptotal = w_bcast<kSolo>(pincl, 31);
     if (ptotal) {
         uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(C.push_ctr, ptotal);
+        if (kSolo) {
+            base = *C.push_ctr;
+            *C.push_ctr = base + ptotal;
+        } else if (lane == 0) {
+            base = atomicAdd(C.push_ctr, ptotal);
+        }
         base = w_bcast<kSolo>(base, 0);
         uint32_t pos = base + pincl - npush;
         if (npush) {
@@ -1256,7 +1282,8 @@ __device__ __forceinline__ void copy_records(uint32_t* dst, const uint32_t* src,
 }
 
 // Collection of a shared-memory resident arena by CTA 0 (the grid-wide
-// gc_compact restated for one CTA): claim refcount-zero slots and follow
+// gc_compact restated for one CTA): recount references (unless the run keeps
+// them), claim refcount-zero slots and follow
 // their cascades to the end, renumber live slots in order (map in the idle
 // frontier list `map`, so the resident arena holds at most kSmallCap
 // slots), move records down chunk by chunk, and remap arguments, waiter
@@ -1264,6 +1291,7 @@ __device__ __forceinline__ void copy_records(uint32_t* dst, const uint32_t* src,
 template <int W>
 __device__ uint32_t local_gc(const Params& P, const Prog& G, Smem& sm, uint32_t* A, uint32_t bump, uint32_t* list,
                              uint32_t m, uint32_t* map) {
+    if (!P.track_rc) recount_refs<W>(P, G, A, bump, threadIdx.x, kBlock, []() { __syncthreads(); });
     for (uint32_t x = 1 + threadIdx.x; x < bump; x += kBlock) {
         uint32_t* R = rec<W>(A, x);
         const uint32_t head = R[kWHead];

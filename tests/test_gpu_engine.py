@@ -267,6 +267,26 @@ def test_trace_records(engine):
     assert engine.live_count() >= 1
 
 
+@pytest.mark.parametrize("name", ["mergesort64_s1", "fib12", "ackermann23", "buildsum8", "fibbatch64_s3"])
+@pytest.mark.parametrize("gc_interval", [0, 2])
+def test_refcounts_recounted_equal_tracked(engine, name, gc_interval):
+    """The step loop keeps refcounts only when validating; collectors and
+    live_count recount them from the store (gc.cuh recount_refs).  Same store
+    either way: the live count (refcount > 0) after a run with the same
+    collection schedule, and a validating run (ghost invariant) on top of an
+    untracked one passes."""
+    s = api.System(CASES[name]["text"])
+    st = api.Store.load(s)
+    engine.set_program(s)
+    counts = []
+    for validate in (1, 0):
+        engine.load(st)
+        engine.run(api.make_options(validate=validate, gc_interval=gc_interval))
+        counts.append(engine.live_count())
+    assert counts[0] == counts[1]
+    engine.run(api.make_options(validate=1))  # recounts the untracked run's store first
+
+
 def _sha(widths):
     return hashlib.sha1(np.asarray(widths, "<u8").tobytes()).hexdigest()
 
