@@ -1914,7 +1914,7 @@ ExportArgs export_args(trs_gpu_engine* e, const Ctl& c) {
     ExportArgs X{};
     uint32_t* scratch = e->d_list[c.cur ^ 1];  // the frontier lives in list[c.cur]
     for (int k = 0; k < 3; ++k) X.queue[k] = scratch + (size_t)k * c.bump;
-    X.map = scratch + (size_t)3 * c.bump;
+    X.map = scratch + (((size_t)c.bump + 3) & ~(size_t)3);  // 16-byte aligned (export.cuh stores quads); queue[1] unused
     X.newrc = e->d_gcmap;
     X.counters = e->d_blocksum + kMaxGrid;
     const ExportStaging st = export_staging(e, c);
@@ -1989,13 +1989,14 @@ int pack_export(trs_gpu_engine* e, const HostColumns* host) {
     const uint8_t* arity = e->d_prog + reinterpret_cast<const ProgHeader*>(e->blob.data())->off_arity;
     if (!e->stream2) CUDA_TRY(e, cudaStreamCreateWithFlags(&e->stream2, cudaStreamNonBlocking));
     const uint32_t B = std::max(1u, e->export_blocks);
-    const uint32_t span = bump > 1 ? bump - 1 : 0, chunk = (span + B - 1) / B;
+    // the export kernel renumbered CTA b's 8-slot groups [b * gchunk, (b + 1) * gchunk)
+    const uint32_t ngroups = (bump + 7) / 8, gchunk = (ngroups + B - 1) / B;
     const uint32_t G = std::min<uint32_t>(8, B);
     uint32_t row = 1;  // row 0 is slot 0 (zeros, written by the export kernel)
     for (uint32_t g = 0; g < G; ++g) {
         const uint32_t b0 = g * B / G, b1 = (g + 1) * B / G;
-        const uint32_t lo = std::min<uint64_t>(bump, 1 + (uint64_t)b0 * chunk);
-        const uint32_t hi = std::min<uint64_t>(bump, 1 + (uint64_t)b1 * chunk);
+        const uint32_t lo = std::max<uint64_t>(1, std::min<uint64_t>(bump, 8ull * b0 * gchunk));
+        const uint32_t hi = std::min<uint64_t>(bump, 8ull * b1 * gchunk);
         uint32_t rows = 0;
         for (uint32_t b = b0; b < b1; ++b) rows += e->export_cta_live[b];
         if (hi > lo) {

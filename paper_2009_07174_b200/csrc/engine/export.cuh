@@ -162,17 +162,32 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
     }
     grid_sync(P.ctl, nblocks, epoch);
     TRS_EXPORT_MARK(1)
-    // renumber live slots in arena order: per-CTA contiguous ranges
-    const uint32_t span = bump - 1;
-    const uint32_t chunk = (span + nblocks - 1) / nblocks;
-    const uint32_t lo = 1 + blockIdx.x * chunk;
-    const uint32_t hi = min(bump, lo + chunk);
-    constexpr uint32_t kPer = 8;  // slots per thread per pass: their loads issue together
-    uint32_t cnt = 0;
-    for (uint32_t y0 = lo + threadIdx.x * kPer; y0 < hi; y0 += kBlock * kPer) {
+    // renumber live slots in arena order: per-CTA contiguous ranges of
+    // 8-slot groups, each thread a group per pass (two 16-byte loads of the
+    // reference counts, two 16-byte stores of the map), one block scan per
+    // 4096 slots
+    const uint32_t ngroups = (bump + 7) / 8;
+    const uint32_t gchunk = (ngroups + nblocks - 1) / nblocks;
+    const uint32_t glo = blockIdx.x * gchunk;
+    const uint32_t ghi = min(ngroups, glo + gchunk);
+    auto live_bits = [&](uint32_t g) -> uint32_t {
+        const uint32_t y = g * 8;
+        uint32_t rc[8];
+        if (y + 8 <= bump) {
+            const uint4 a = __ldcg(reinterpret_cast<const uint4*>(X.newrc + y));
+            const uint4 b = __ldcg(reinterpret_cast<const uint4*>(X.newrc + y + 4));
+            rc[0] = a.x, rc[1] = a.y, rc[2] = a.z, rc[3] = a.w, rc[4] = b.x, rc[5] = b.y, rc[6] = b.z, rc[7] = b.w;
+        } else {
 #pragma unroll
-        for (uint32_t k = 0; k < kPer; ++k) cnt += (y0 + k < hi && __ldcg(X.newrc + y0 + k) != 0u) ? 1u : 0u;
-    }
+            for (uint32_t k = 0; k < 8; ++k) rc[k] = y + k < bump ? __ldcg(X.newrc + y + k) : 0u;
+        }
+        uint32_t bits = 0;
+#pragma unroll
+        for (uint32_t k = 0; k < 8; ++k) bits |= (rc[k] != 0u ? 1u : 0u) << k;
+        return y == 0 ? bits & ~1u : bits;  // slot 0 is never live
+    };
+    uint32_t cnt = 0;
+    for (uint32_t g = glo + threadIdx.x; g < ghi; g += kBlock) cnt += __popc(live_bits(g));
     uint32_t tot;
     block_scan(cnt, &tot, sm);
     if (threadIdx.x == 0) P.blocksum[blockIdx.x] = tot;
@@ -190,20 +205,28 @@ __global__ void __launch_bounds__(kBlock, 1) export_store(Params P, ExportArgs X
         prefix = t1;
         all = t2;
     }
-    // eight consecutive slots per thread: one block scan per 4096 slots
     uint32_t running = 1 + prefix;
-    for (uint32_t y0 = lo; y0 < hi; y0 += kBlock * kPer) {
-        const uint32_t yb = y0 + threadIdx.x * kPer;
-        uint32_t live = 0;  // bit k: slot yb + k is live
-#pragma unroll
-        for (uint32_t k = 0; k < kPer; ++k)
-            if (yb + k < hi && __ldcg(X.newrc + yb + k) != 0u) live |= 1u << k;
+    for (uint32_t g0 = glo; g0 < ghi; g0 += kBlock) {
+        const uint32_t g = g0 + threadIdx.x;
+        const uint32_t live = g < ghi ? live_bits(g) : 0u;  // bit k: slot 8g + k is live
         uint32_t t;
         uint32_t e = running + block_scan(__popc(live), &t, sm);
+        if (g < ghi) {
+            uint32_t m[8];
 #pragma unroll
-        for (uint32_t k = 0; k < kPer; ++k) {
-            if (yb + k < hi) X.map[yb + k] = ((live >> k) & 1u) ? e : 0u;
-            e += (live >> k) & 1u;
+            for (uint32_t k = 0; k < 8; ++k) {
+                m[k] = ((live >> k) & 1u) ? e : 0u;
+                e += (live >> k) & 1u;
+            }
+            const uint32_t y = g * 8;
+            if (y + 8 <= bump) {
+                *reinterpret_cast<uint4*>(X.map + y) = make_uint4(m[0], m[1], m[2], m[3]);
+                *reinterpret_cast<uint4*>(X.map + y + 4) = make_uint4(m[4], m[5], m[6], m[7]);
+            } else {
+#pragma unroll
+                for (uint32_t k = 0; k < 8; ++k)
+                    if (y + k < bump) X.map[y + k] = m[k];
+            }
         }
         running += t;
     }

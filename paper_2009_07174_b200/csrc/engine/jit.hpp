@@ -219,7 +219,11 @@ struct JitResult {
 inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     static std::mutex mu;
     static std::unordered_map<std::string, std::pair<const void*, const void*>> cache;
-    const std::string key = std::to_string(W) + "/" + std::to_string(minb) + (TRS_B200_PROFILE ? "p\n" : "\n") + src;
+    // compile-time knobs for A/B experiments (e.g. "-DTRS_B200_RA_PREFETCH=0"), space separated
+    const char* defs_env = std::getenv("TRS_B200_JIT_DEFINES");
+    const std::string defs = defs_env ? defs_env : "";
+    const std::string key =
+        std::to_string(W) + "/" + std::to_string(minb) + (TRS_B200_PROFILE ? "p" : "") + defs + "\n" + src;
     {
         std::lock_guard<std::mutex> g(mu);
         auto it = cache.find(key);
@@ -238,9 +242,19 @@ inline JitResult jit_compile(const std::string& src, int W, int minb = 1) {
     nvrtcAddNameExpression(prog, name_ra.c_str());
     // the specialisation is built like the library that loads it (profiling build or not)
     const char* verbose = std::getenv("TRS_B200_JIT_VERBOSE");  // ptxas register/spill report in the log
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
-                          TRS_B200_PROFILE ? "-DTRS_B200_PROFILE=1" : "-DTRS_B200_PROFILE=0", "--ptxas-options=-v"};
-    const nvrtcResult rc = nvrtcCompileProgram(prog, (verbose && verbose[0] == '1') ? 5 : 4, opts);
+    std::vector<std::string> extra;
+    for (size_t a = 0; a < defs.size();) {
+        const size_t b = defs.find(' ', a);
+        const std::string t = defs.substr(a, b == std::string::npos ? std::string::npos : b - a);
+        if (!t.empty()) extra.push_back(t);
+        if (b == std::string::npos) break;
+        a = b + 1;
+    }
+    std::vector<const char*> opts = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                                     TRS_B200_PROFILE ? "-DTRS_B200_PROFILE=1" : "-DTRS_B200_PROFILE=0"};
+    for (const std::string& t : extra) opts.push_back(t.c_str());
+    if (verbose && verbose[0] == '1') opts.push_back("--ptxas-options=-v");
+    const nvrtcResult rc = nvrtcCompileProgram(prog, (int)opts.size(), opts.data());
     size_t n = 0;
     nvrtcGetProgramLogSize(prog, &n);
     out.log.resize(n);

@@ -143,6 +143,9 @@ constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
 #ifndef TRS_B200_RICH_ENTRIES
 #define TRS_B200_RICH_ENTRIES 0
 #endif
+#ifndef TRS_B200_RA_PREFETCH
+#define TRS_B200_RA_PREFETCH 1
+#endif
 
 struct PhaseClock {
     long long t[4] = {0, 0, 0, 0};  // match, claim, apply, push (debug accounting)
@@ -303,6 +306,17 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             }
         }
         if (prof) pc.mark(1, cep[0] ^ cep[MAXA - 1] ^ ca[0]);
+        // run-ahead in a grid sweep: a lane that carries on into a node it
+        // builds from these grandchildren (a spine, Plus(S(X), Y) ->
+        // S(Plus(X, Y))) reads their records in its next step: start those
+        // misses now (words past an arity are slot 0).  Grid sweeps only: the
+        // single-CTA modes' chains run from L1 or the resident arena, where
+        // the extra instructions measured slower (tools/knob_ab.py)
+        if (kRA && !kSolo && !C.lone && may_cont && C.cont_room && TRS_B200_RA_PREFETCH) {
+#pragma unroll
+            for (int q = 0; q < (int)kPlanChildren * 4; ++q)
+                if (ca[q]) asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, ca[q])));
+        }
         // Logical derive sweep (oracle_logical): one past the slot's build or
         // last rewrite, and past every argument's nf epoch.  An argument that
         // is not nf -- or whose nf is too fresh to read: published in this

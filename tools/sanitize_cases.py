@@ -1,7 +1,7 @@
 """Small normalisations for compute-sanitizer runs (tools/sanitize.sh): the
 golden unit and family cases and random programs, in the default
 (run-ahead), synchronous, grid-only, interpreted and collect-every-sweep
-modes, each checked against its fixture or the oracle so that a run that
+(refcounts kept, or recounted by the collector) modes, each checked against its fixture or the oracle so that a run that
 the sanitizer lets through is also a correct one."""
 import json
 import os
@@ -17,7 +17,9 @@ from paper_2009_07174_b200 import api  # noqa: E402
 from paper_2009_07174_b200 import workloads as W  # noqa: E402
 
 MODES = {"default": {}, "sync": {"no_runahead": 1}, "grid": {"disable_small": 1},
-         "interp": {"interpreted": 1}, "gc1": {"gc_interval": 1, "validate": 1}, "validate2": {"validate": 2}}
+         "interp": {"interpreted": 1}, "gc1": {"gc_interval": 1, "validate": 1},
+         "gc1u": {"gc_interval": 1},  # collect every sweep, refcounts recounted by the collector
+         "validate2": {"validate": 2}}
 
 
 def main():
