@@ -911,6 +911,9 @@ int alloc_store(trs_gpu_engine* e, uint64_t capacity) {
     for (int k = 0; k < 2; ++k) {
         CUDA_TRY(e, cudaMalloc(&e->d_arena[k], rec_bytes * capacity));
         CUDA_TRY(e, cudaMalloc(&e->d_list[k], sizeof(uint32_t) * e->W * capacity));
+        // once per allocation: record words past an arity are never written, but
+        // whole-record copies (resident arena, compaction) move them
+        CUDA_TRY(e, cudaMemsetAsync(e->d_arena[k], 0, rec_bytes * capacity, e->stream));
     }
     CUDA_TRY(e, cudaMalloc(&e->d_gcmap, sizeof(uint32_t) * capacity));
     e->capacity = capacity;
@@ -992,6 +995,7 @@ int grow_store(trs_gpu_engine* e, uint64_t needed) {
     }
     // the frontier of the next sweep: regions of list buffer c.cur
     uint64_t extent = frontier_extent(e, c);
+    for (int k = 0; k < 2; ++k) CUDA_TRY(e, cudaMemsetAsync(na[k], 0, rec_bytes * cap, e->stream));
     CUDA_TRY(e, cudaMemcpyAsync(na[c.arena], e->d_arena[c.arena], rec_bytes * c.bump, cudaMemcpyDeviceToDevice, e->stream));
     // frontier entries are one word (bare slots) or a record (rich entries)
     const size_t entry_bytes = e->rich ? rec_bytes : sizeof(uint32_t);
