@@ -40,6 +40,13 @@ __device__ __forceinline__ uint32_t* bind_base(const Params& P, uint32_t* slist)
 
 enum Act : uint32_t { kActNone = 0, kActWait, kActNf, kActCollapse, kActBuild, kActDefer, kActChain };
 
+// The slot a lane last published nf in this physical sweep, with the head
+// and epoch words it wrote (run-ahead: its parent is usually the lane's next
+// step, and reads them without a round trip)
+struct NfCarry {
+    uint32_t slot, head, epoch;
+};
+
 struct Slab {
     uint32_t cur, end;  // warp-uniform: [cur, end) are this warp's unused fresh slots
     uint32_t room;      // warp-uniform: the sweep's claims leave room for run-ahead
@@ -143,6 +150,15 @@ constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
 #ifndef TRS_B200_RICH_ENTRIES
 #define TRS_B200_RICH_ENTRIES 0
 #endif
+#ifndef TRS_B200_LONE
+#define TRS_B200_LONE 1
+#endif
+#ifndef TRS_B200_PUB_FAST
+#define TRS_B200_PUB_FAST 1
+#endif
+#ifndef TRS_B200_NF_CARRY
+#define TRS_B200_NF_CARRY 1
+#endif
 #ifndef TRS_B200_RA_PREFETCH
 #define TRS_B200_RA_PREFETCH 1
 #endif
@@ -178,12 +194,15 @@ constexpr uint32_t kEntHasPayload = 1;
 // kRA: the run-ahead build of the step loop (continuations, publication
 // stamps, logical derive sweeps); without it logical and physical sweeps
 // coincide and the step is the lean synchronous one.
-template <int W, bool kRich, bool kRA, bool kSolo = false>
+template <int W, bool kRich, bool kRA, int kSolo = 0>
 __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, uint32_t* arena, const StepCtx& C,
                                               Slab& slab, bool valid, const uint32_t* entry, bool prof_req,
                                               PhaseClock& pc, bool may_cont, uint32_t& cont, uint32_t& tmax,
-                                              uint32_t& just_nf, uint32_t& pushes) {
+                                              NfCarry& just_nf, uint32_t& pushes) {
     const bool prof = kProfBuild && prof_req;
+    // kSolo 1: lane 0 alone on the device (plain counters); 2: one lane of
+    // its warp in a grid sweep (atomics, but no warp collectives)
+    constexpr bool kAlone = kSolo != 0;
     constexpr int MAXA = rec_args(W);
     // arguments any symbol of the program has: the specialisation knows it,
     // so loops over arguments stop there and their registers disappear
@@ -298,6 +317,11 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                     ca[j * 4 + 1] = q1.y;
                     ca[j * 4 + 2] = q1.z;
                     ca[j * 4 + 3] = q1.w;
+                } else if (kRA && TRS_B200_NF_CARRY && a[j] == just_nf.slot) {
+                    // the argument this lane has just made nf: its head and
+                    // epoch are in registers (an nf record no longer changes)
+                    ch[j] = just_nf.head;
+                    cep[j] = just_nf.epoch;
                 } else {
                     const uint2 c = *reinterpret_cast<const uint2*>(C);
                     ch[j] = c.x & kSymMask;
@@ -312,7 +336,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         // misses now (words past an arity are slot 0).  Grid sweeps only: the
         // single-CTA modes' chains run from L1 or the resident arena, where
         // the extra instructions measured slower (tools/knob_ab.py)
-        if (kRA && !kSolo && !C.lone && may_cont && C.cont_room && TRS_B200_RA_PREFETCH) {
+        if (kRA && kSolo != 1 && !C.lone && may_cont && C.cont_room && TRS_B200_RA_PREFETCH) {
 #pragma unroll
             for (int q = 0; q < (int)kPlanChildren * 4; ++q)
                 if (ca[q]) asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, ca[q])));
@@ -333,7 +357,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             if ((uint32_t)j < ar) {
                 const uint32_t e = cep[j];
                 const bool ready = epoch_nf(e) && (kRA ? (((e >> kEpochBits) & kStampMask) != C.stamp ||
-                                                          a[j] == just_nf)
+                                                          a[j] == just_nf.slot)
                                                        : (e & kEpochMask) < s);
                 if (kRA && ready) T = max(T, (e & kEpochMask) + 1);
                 if (!ready) {
@@ -540,29 +564,29 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 
     // ---- claim fresh slots from the warp's slab
     const uint32_t need = act == kActBuild ? G.rules[rule].new_slots : 0;
-    const uint32_t incl = w_scan<kSolo>(need);
-    const uint32_t total = w_bcast<kSolo>(incl, 31);
+    const uint32_t incl = w_scan<kAlone>(need);
+    const uint32_t total = w_bcast<kAlone>(incl, 31);
     uint32_t fresh = 0;
     if (total) {
         if (slab.end - slab.cur < total) {
-            abandon_slab<W, kSolo>(arena, slab);
+            abandon_slab<W, kAlone>(arena, slab);
             const uint32_t size = max(C.slab, total);
             uint32_t off = 0;
-            if (kSolo) {
+            if (kSolo == 1) {
                 // the solo step runs alone on the device: plain counters
                 off = *C.claim_ctr;
                 *C.claim_ctr = off + size;
-            } else if (lane == 0) {
+            } else if (kAlone || lane == 0) {
                 off = atomicAdd(C.claim_ctr, size);
             }
-            off = w_bcast<kSolo>(off, 0);
+            off = w_bcast<kAlone>(off, 0);
             // run-ahead feeds on the slots the sweep's worst case leaves over
             if (kRA) slab.room = (uint64_t)off + size <= C.claim_soft ? 1u : 0u;
             const uint64_t start = (uint64_t)C.bump + off;
             if (start + total > C.cap) {
                 // not even this step's slots fit: the reference raises
                 // Capacity when get_new_index finds no slot (sweep_engine.cpp:221-226)
-                if (lane == 0) {
+                if (kAlone || lane == 0) {
                     atomicExch(&P.ctl->abort_capacity, 1u);
                     atomicOr(C.flags, kFlagCapacity);
                 }
@@ -606,7 +630,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
             R[kWEpoch] = T | (C.stamp << kEpochBits);
         }
         tmax = max(tmax, T + chain_k);
-        if (kRA) just_nf = i;
+        if (kRA) just_nf = NfCarry{i, chain_k ? chain_f : sym, (T + chain_k) | (C.stamp << kEpochBits)};
         wword = R + kWWaiter;
         wcmp = own_waiter;
         wval = kWoken;
@@ -653,12 +677,12 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         uint32_t* R = rec<W>(arena, i);
         *reinterpret_cast<uint2*>(R) = make_uint2(shead, T | (C.stamp << kEpochBits));
         tmax = max(tmax, T);
-        if (kRA) just_nf = i;
+        if (kRA) just_nf = NfCarry{i, shead, T | (C.stamp << kEpochBits)};
         store_args<W>(R, b, ar > sar ? ar : sar);
 #pragma unroll
         for (int j = 0; j < MAXA; ++j) {
             if ((uint32_t)j >= sar) break;
-            if (P.track_rc) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
+            if (P.track_rc) rc_upd<kAlone>(rec<W>(arena, b[j]) + kWRc, 1);
         }
         wword = R + kWWaiter;
         wcmp = own_waiter;
@@ -667,7 +691,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     } else if (act == kActBuild) {
         const DRule& Rl = G.rules[rule];
 #if TRS_GEN
-        gen_build<W, kSolo>(rule, arena, fresh, i, ar, gb, kTminBit | (T + 1), P.track_rc != 0);
+        gen_build<W, kAlone>(rule, arena, fresh, i, ar, gb, kTminBit | (T + 1), P.track_rc != 0);
 #else
         const uint32_t nfresh = Rl.new_slots;
         for (uint32_t k = 0; k <= nfresh; ++k) {
@@ -711,7 +735,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
             for (int j = 0; j < AE; ++j) {
                 if ((vmask >> j) == 0u) break;
-                if (((vmask >> j) & 1u) && P.track_rc) rc_upd<kSolo>(rec<W>(arena, b[j]) + kWRc, 1);
+                if (((vmask >> j) & 1u) && P.track_rc) rc_upd<kAlone>(rec<W>(arena, b[j]) + kWRc, 1);
             }
         }
 #endif
@@ -729,7 +753,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 #pragma unroll
         for (int j = 0; j < AE; ++j) {
             if ((uint32_t)j >= ar) break;
-            rc_upd<kSolo>(rec<W>(arena, a[j]) + kWRc, -1);
+            rc_upd<kAlone>(rec<W>(arena, a[j]) + kWRc, -1);
         }
     }
     uint32_t wake = 0;  // the parent this lane's nf publication woke
@@ -740,12 +764,18 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         if (kRA && act != kActWait && own_waiter != 0u && own_waiter != kWoken)
             asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, own_waiter)));  // generic: no-op on the resident arena
         uint32_t old;
-        if (kSolo) {
+        if (kSolo == 1) {
             // nothing else runs: the subscription and the publication are a
             // read and a write (an nf publication's word is the one loaded
             // with the record, unchanged since: only subscribers write it)
             old = act == kActWait ? *wword : wcmp;
             if (old == wcmp) *wword = wval;
+        } else if (TRS_B200_PUB_FAST && act != kActWait && wcmp != 0u && wcmp != kWoken) {
+            // the word held a subscriber when the record was loaded, and a
+            // word holding a subscriber changes only by this publication
+            // (a later subscriber's CAS expects 0): the swap needs no answer
+            atomicExch(wword, kWoken);
+            old = wcmp;
         } else {
             old = atomicCAS(wword, wcmp, wval);
         }
@@ -776,16 +806,16 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     bool want = kRA && may_cont && slab.room != 0u &&
                 (wake != 0u || ((act == kActBuild || act == kActChain) && (push_mask != 0u || root_push)));
     if (kRA && C.cont_room) {
-        const uint32_t wm = kSolo ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
+        const uint32_t wm = kAlone ? (want ? 1u : 0u) : __ballot_sync(0xffffffffu, want);
         if (wm) {
             uint32_t ok = 0;
-            if (kSolo) {
+            if (kSolo == 1) {
                 const int need = (int)C.cont_cost;
                 if (*C.cont_room >= need) {
                     *C.cont_room -= need;
                     ok = 1;
                 }
-            } else if (lane == 0) {
+            } else if (kAlone || lane == 0) {
                 const int need = __popc(wm) * (int)C.cont_cost;
                 const int before = atomicSub(C.cont_room, need);
                 if (before >= need)
@@ -793,7 +823,7 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
                 else
                     atomicAdd(C.cont_room, need);
             }
-            if (!w_bcast<kSolo>(ok, 0)) want = false;
+            if (!w_bcast<kAlone>(ok, 0)) want = false;
         }
     } else {
         want = false;
@@ -827,17 +857,17 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
 
     pushes += npush;
     // ---- next frontier: one shared-memory reservation per warp step
-    const uint32_t pincl = w_scan<kSolo>(npush);
-    const uint32_t ptotal = w_bcast<kSolo>(pincl, 31);
+    const uint32_t pincl = w_scan<kAlone>(npush);
+    const uint32_t ptotal = w_bcast<kAlone>(pincl, 31);
     if (ptotal) {
         uint32_t base = 0;
-        if (kSolo) {
+        if (kSolo == 1) {
             base = *C.push_ctr;
             *C.push_ctr = base + ptotal;
-        } else if (lane == 0) {
+        } else if (kAlone || lane == 0) {
             base = atomicAdd(C.push_ctr, ptotal);
         }
-        base = w_bcast<kSolo>(base, 0);
+        base = w_bcast<kAlone>(base, 0);
         uint32_t pos = base + pincl - npush;
         if (npush) {
             if (act == kActBuild) {
@@ -899,20 +929,20 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
     // the lanes of a warp on the same chain add together)
     uint32_t nrw = rewrote ? (chain_k ? chain_k : 1u) : 0u;
     if (kRA) {
-        const uint32_t steps = kSolo ? nrw : __reduce_max_sync(0xffffffffu, nrw);
+        const uint32_t steps = kAlone ? nrw : __reduce_max_sync(0xffffffffu, nrw);
         for (uint32_t j = 0; j < steps; ++j) {
             const bool on = j < nrw;
             const uint32_t Tj = T + j;
             if (C.hwin) {
                 const bool win = on && Tj - C.hbase < kHistWin;
-                hist_add<kSolo>(C.hwin + (Tj - C.hbase), win);
-                hist_add<kSolo>(C.hist + (Tj - C.t0), on && !win);
+                hist_add<kAlone>(C.hwin + (Tj - C.hbase), win);
+                hist_add<kAlone>(C.hist + (Tj - C.t0), on && !win);
             } else {
-                hist_add<kSolo>(C.hist + (Tj - C.t0), on);
+                hist_add<kAlone>(C.hist + (Tj - C.t0), on);
             }
         }
     }
-    if (kSolo) return nrw;
+    if (kAlone) return nrw;
     return kRA ? __reduce_add_sync(0xffffffffu, nrw) : __popc(__ballot_sync(0xffffffffu, rewrote));
 }
 
@@ -942,7 +972,8 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     const uint32_t gw = nblocks * kWarps;
     const uint32_t q = chunk_lanes(F.M, nblocks);
     unsigned long long rw = 0;
-    uint32_t cont = 0, just_nf = 0, pushes = 0;
+    uint32_t cont = 0, pushes = 0;
+    NfCarry just_nf{};
     if (kRich) {
         for (uint32_t k = block_rank * kWarps + warp; k * q < F.M; k += gw) {
             const uint32_t v = k * q + lane;
@@ -982,7 +1013,34 @@ __device__ __forceinline__ unsigned long long cta_entries(const Params& P, const
     uint32_t steps = 0;
     for (;;) {
         const bool own = lane < q && k * q + lane < F.M;
-        if (!__any_sync(0xffffffffu, cont != 0u || own)) break;
+        const uint32_t busy = __ballot_sync(0xffffffffu, cont != 0u || own);
+        if (!busy) break;
+#if TRS_B200_LONE
+        // A lone chain: one lane of the warp has work, and it is a
+        // continuation.  It runs its chain without warp collectives (the
+        // tails of the batches: a few chains per warp, one step per logical
+        // sweep, the step's path length is the critical path), then hands
+        // the warp-uniform slab state back.
+        if (W == 8 && __popc(busy) == 1 && (busy & __ballot_sync(0xffffffffu, cont != 0u))) {
+            uint32_t lrw = 0;
+            if (cont) {
+                do {
+                    ++steps;
+                    uint32_t slot = cont;
+                    lrw += warp_step<W, kRich, kRA, 2>(P, G, arena, C, slab, true, &slot,
+                                                       prof && (TRS_B200_PROFILE || warp == 0), pc,
+                                                       ra_more(P, C, steps), cont, tmax, just_nf, pushes);
+                } while (cont);
+            }
+            const int src = __ffs(busy) - 1;
+            lrw = __shfl_sync(0xffffffffu, lrw, src);
+            if (lane == 0) rw += lrw;
+            slab.cur = __shfl_sync(0xffffffffu, slab.cur, src);
+            slab.end = __shfl_sync(0xffffffffu, slab.end, src);
+            slab.room = __shfl_sync(0xffffffffu, slab.room, src);
+            continue;
+        }
+#endif
         uint32_t slot = cont;
         if (cont) {
             ++steps;
@@ -1407,10 +1465,11 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
                     ss.cont_room = (int)(kSmallCap - (P.max_new + 1));
                     const StepCtx C = make_ctx(P, L, s, &ss.claim, slist + (sc1 ^ 1) * kSmallCap, &ss.count[sc1 ^ 1],
                                                &ss.flags, cap, slab_size, slist, 1, 1, &ss.cont_room);
-                    uint32_t width = 0, cont = 0, steps = 0, just_nf = 0, pushes = 0;
+                    uint32_t width = 0, cont = 0, steps = 0, pushes = 0;
+                    NfCarry just_nf{};
                     uint32_t slot = slist[sc1 * kSmallCap];
                     for (;;) {
-                        width += warp_step<W, false, kRA, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                        width += warp_step<W, false, kRA, 1>(P, G, arena, C, slab, true, &slot, prof, pc,
                                                            ra_more(P, C, steps), cont, tmax, just_nf, pushes);
                         if (!cont) break;
                         slot = cont;
@@ -1470,10 +1529,11 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             // one entry, specialised wide-record kernel: lane 0 alone for this sweep
             uint32_t w1 = 0;
             if (lane == 0) {
-                uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
+                uint32_t cont = 0, steps = 0, pushes = 0;
+                NfCarry just_nf{};
                 uint32_t slot = slist[sc * kSmallCap];
                 for (;;) {
-                    w1 += warp_step<W, false, kRA, true>(P, G, arena, C, slab, true, &slot, prof, pc,
+                    w1 += warp_step<W, false, kRA, 1>(P, G, arena, C, slab, true, &slot, prof, pc,
                                                     ra_more(P, C, steps), cont, tmax, just_nf, pushes);
                     if (!cont) break;
                     slot = cont;
@@ -1485,12 +1545,35 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
             slab.end = __shfl_sync(0xffffffffu, slab.end, 0);
             slab.room = __shfl_sync(0xffffffffu, slab.room, 0);
         } else {
-            uint32_t cont = 0, steps = 0, just_nf = 0, pushes = 0;
+            uint32_t cont = 0, steps = 0, pushes = 0;
+            NfCarry just_nf{};
             uint32_t slot = lane < m ? slist[sc * kSmallCap + lane] : 0u;
             for (;;) {
                 width += warp_step<W, false, kRA>(P, G, arena, C, slab, slot != 0u, &slot, prof, pc,
                                              ra_more(P, C, steps), cont, tmax, just_nf, pushes);
-                if (!__any_sync(0xffffffffu, cont != 0u)) break;
+                const uint32_t cm = __ballot_sync(0xffffffffu, cont != 0u);
+                if (!cm) break;
+#if TRS_B200_LONE
+                if (W == 8 && kRA && __popc(cm) == 1) {
+                    // one chain left: its lane runs it alone (the rest of
+                    // the device is idle in warp mode: plain counters)
+                    uint32_t lw = 0;
+                    if (cont) {
+                        do {
+                            ++steps;
+                            uint32_t sl = cont;
+                            lw += warp_step<W, false, kRA, 1>(P, G, arena, C, slab, true, &sl, prof, pc,
+                                                              ra_more(P, C, steps), cont, tmax, just_nf, pushes);
+                        } while (cont);
+                    }
+                    const int src = __ffs(cm) - 1;
+                    width += __shfl_sync(0xffffffffu, lw, src);
+                    slab.cur = __shfl_sync(0xffffffffu, slab.cur, src);
+                    slab.end = __shfl_sync(0xffffffffu, slab.end, src);
+                    slab.room = __shfl_sync(0xffffffffu, slab.room, src);
+                    break;
+                }
+#endif
                 slot = cont;
                 ++steps;
             }
