@@ -135,6 +135,7 @@ struct Params {
     uint32_t validate;      // 2: quiescent-point scans before every grid sweep (validate.cuh)
     uint32_t* val;          // their scratch, 3 words per slot
     uint32_t track_rc;      // steps keep refcounts (validate modes); otherwise collectors recount (gc.cuh)
+    uint32_t ra_warm_past;  // ra_warm once the frontier is below an eighth of the widest sweep so far
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

@@ -1504,6 +1504,8 @@ int enqueue_launch(trs_gpu_engine* e) {
         P.ra_kill = rk ? (uint32_t)std::strtoul(rk, nullptr, 10) : (uint32_t)R.blocks * kWarps * 64u;
         const char* rw = std::getenv("TRS_B200_RA_WARM");
         P.ra_warm = rw ? (uint32_t)std::strtoul(rw, nullptr, 10) : 64u;
+        const char* rp = std::getenv("TRS_B200_RA_WARM_PAST");
+        P.ra_warm_past = rp ? (uint32_t)std::strtoul(rp, nullptr, 10) : 64u;
         const char* rs = std::getenv("TRS_B200_RA_STEPS");
         P.ra_steps = rs ? (uint32_t)std::strtoul(rs, nullptr, 10) : 32u;
         // refcounts are kept step by step only for the validate modes (their

@@ -1293,6 +1293,14 @@ struct SmallState {
 // out of step, and a warp of lanes on different rules diverges.
 // The lean (synchronous) build returns true instead: it hands the run over
 // to the run-ahead build (kNeedRA), which switches on at its first sweep.
+// Past the run's widest sweep (the frontier below an eighth of it: the
+// shrinking phase, whose chains only get longer), the hand-over waits
+// P.ra_warm_past sweeps instead; a growing phase keeps the full P.ra_warm (a
+// wide phase after run-ahead measured slower, build+sum and transform).
+__device__ __forceinline__ uint32_t ra_warm_now(const Params& P, const Local& L, uint32_t m) {
+    return (unsigned long long)m * 8u < L.maxw ? min(P.ra_warm, P.ra_warm_past) : P.ra_warm;
+}
+
 template <bool kRA>
 __device__ __forceinline__ bool ra_track(const Params& P, Local& L, uint32_t m) {
     if (!P.runahead) return false;
@@ -1301,8 +1309,9 @@ __device__ __forceinline__ bool ra_track(const Params& P, Local& L, uint32_t m) 
         L.ra_on = 0;
         return false;
     }
-    if (L.ra_narrow < P.ra_warm) ++L.ra_narrow;
-    if (L.ra_narrow < P.ra_warm) return false;
+    const uint32_t warm = ra_warm_now(P, L, m);
+    if (L.ra_narrow < warm) ++L.ra_narrow;
+    if (L.ra_narrow < warm) return false;
     if (!kRA) return true;
     L.ra_on = 1;
     L.ra_used = 1;
@@ -1887,7 +1896,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             load_local(L, ctl);
             F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
-            if (!kRA && P.runahead && L.ra_narrow >= P.ra_warm) {
+            if (!kRA && P.runahead && L.ra_narrow >= ra_warm_now(P, L, F.M)) {
                 exit_status = kNeedRA;
                 break;
             }
