@@ -75,6 +75,7 @@ struct Ctl {
     uint32_t need_hist;       // a slot's derive sweep lies past the width histogram
     uint32_t hist_need;       // the histogram entries it needs
     uint32_t ra_narrow, ra_on, ra_used;  // run-ahead state (sweep.cuh, ra_track)
+    uint32_t ra_mref, ra_sref, ra_go;    // shrinking-phase window (sweep.cuh, ra_track)
     uint32_t val_kind, val_slot;         // first validate=2 violation (validate.cuh)
     // phase cycle accounting (Params::profile): match, claim, apply, push,
     // sweep, sweeps, warp steps (chunks) of the profiled warp, spare, then
@@ -135,7 +136,7 @@ struct Params {
     uint32_t validate;      // 2: quiescent-point scans before every grid sweep (validate.cuh)
     uint32_t* val;          // their scratch, 3 words per slot
     uint32_t track_rc;      // steps keep refcounts (validate modes); otherwise collectors recount (gc.cuh)
-    uint32_t ra_warm_past;  // ra_warm once the frontier is below an eighth of the widest sweep so far
+    uint32_t ra_warm_past;  // hand-over after this many sweeps of a steady frontier past the widest sweep
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

@@ -189,6 +189,9 @@ __global__ void prep_launch(Ctl* c, uint32_t* claim_ctrs, uint32_t* region_flags
             c->ra_narrow = 0;
             c->ra_on = 0;
             c->ra_used = 0;
+            c->ra_mref = 0;
+            c->ra_sref = 0;
+            c->ra_go = 0;
             c->val_kind = 0;
             c->val_slot = 0;
         }
@@ -1505,7 +1508,7 @@ int enqueue_launch(trs_gpu_engine* e) {
         const char* rw = std::getenv("TRS_B200_RA_WARM");
         P.ra_warm = rw ? (uint32_t)std::strtoul(rw, nullptr, 10) : 64u;
         const char* rp = std::getenv("TRS_B200_RA_WARM_PAST");
-        P.ra_warm_past = rp ? (uint32_t)std::strtoul(rp, nullptr, 10) : 64u;
+        P.ra_warm_past = rp ? (uint32_t)std::strtoul(rp, nullptr, 10) : 16u;
         const char* rs = std::getenv("TRS_B200_RA_STEPS");
         P.ra_steps = rs ? (uint32_t)std::strtoul(rs, nullptr, 10) : 32u;
         // refcounts are kept step by step only for the validate modes (their

@@ -1074,6 +1074,9 @@ struct Local {
     // once it has run, argument readiness is judged by publication stamps
     // (logical and physical sweeps no longer coincide)
     uint32_t ra_narrow, ra_on, ra_used;
+    // a steady frontier past the widest sweep (chains, not a reduction):
+    // the window's widest frontier and first sweep; ra_go: hand over now
+    uint32_t ra_mref, ra_sref, ra_go;
 };
 
 __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
@@ -1092,6 +1095,9 @@ __device__ __forceinline__ void load_local(Local& L, Ctl* c) {
     L.ra_narrow = __ldcg(&c->ra_narrow);
     L.ra_on = __ldcg(&c->ra_on);
     L.ra_used = __ldcg(&c->ra_used);
+    L.ra_mref = __ldcg(&c->ra_mref);
+    L.ra_sref = __ldcg(&c->ra_sref);
+    L.ra_go = __ldcg(&c->ra_go);
 }
 
 __device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
@@ -1109,6 +1115,9 @@ __device__ __forceinline__ void store_local(const Local& L, Ctl* c) {
     c->ra_narrow = L.ra_narrow;
     c->ra_on = L.ra_on;
     c->ra_used = L.ra_used;
+    c->ra_mref = L.ra_mref;
+    c->ra_sref = L.ra_sref;
+    c->ra_go = L.ra_go;
     __threadfence();
 }
 
@@ -1293,25 +1302,35 @@ struct SmallState {
 // out of step, and a warp of lanes on different rules diverges.
 // The lean (synchronous) build returns true instead: it hands the run over
 // to the run-ahead build (kNeedRA), which switches on at its first sweep.
-// Past the run's widest sweep (the frontier below an eighth of it: the
-// shrinking phase, whose chains only get longer), the hand-over waits
-// P.ra_warm_past sweeps instead; a growing phase keeps the full P.ra_warm (a
-// wide phase after run-ahead measured slower, build+sum and transform).
-__device__ __forceinline__ uint32_t ra_warm_now(const Params& P, const Local& L, uint32_t m) {
-    return (unsigned long long)m * 8u < L.maxw ? min(P.ra_warm, P.ra_warm_past) : P.ra_warm;
+// An earlier hand-over, after P.ra_warm_past sweeps, applies to a steady
+// frontier past the run's widest sweep: below an eighth of it and level
+// within 1/16 over the window -- chains advancing one step per sweep, none
+// ending (the plateaus of the batches' tails).  A reduction tree's frontier
+// decays as its chains end at different sweeps, and keeps the full
+// P.ra_warm: its lanes would run ahead only to poll at the next join
+// (build+sum measured 15-28 % slower with a looser test).
+__device__ __forceinline__ bool ra_steady(const Params& P, Local& L, uint32_t m) {
+    const bool past = (unsigned long long)m * 8u < L.maxw;
+    if (!past || m > L.ra_mref || (unsigned long long)m * 16u < (unsigned long long)L.ra_mref * 15u) {
+        L.ra_mref = m;
+        L.ra_sref = L.sweep;
+        return false;
+    }
+    return L.sweep - L.ra_sref >= P.ra_warm_past;
 }
 
 template <bool kRA>
 __device__ __forceinline__ bool ra_track(const Params& P, Local& L, uint32_t m) {
     if (!P.runahead) return false;
+    const bool steady = ra_steady(P, L, m);
     if (m > P.ra_kill) {
         L.ra_narrow = 0;
         L.ra_on = 0;
         return false;
     }
-    const uint32_t warm = ra_warm_now(P, L, m);
-    if (L.ra_narrow < warm) ++L.ra_narrow;
-    if (L.ra_narrow < warm) return false;
+    if (L.ra_narrow < P.ra_warm) ++L.ra_narrow;
+    if (L.ra_narrow < P.ra_warm && !(steady && L.ra_narrow >= P.ra_warm_past)) return false;
+    L.ra_go = 1;
     if (!kRA) return true;
     L.ra_on = 1;
     L.ra_used = 1;
@@ -1896,7 +1915,7 @@ __global__ void __launch_bounds__(kBlock, MINB) step_loop(Params P) {
             load_local(L, ctl);
             F = stage_frontier(P, L.cur, nblocks, f_pref, f_off, sm, nullptr);
             if (L.sweep != before) just_collected = false;  // keep every CTA's plan identical
-            if (!kRA && P.runahead && L.ra_narrow >= ra_warm_now(P, L, F.M)) {
+            if (!kRA && P.runahead && L.ra_go) {
                 exit_status = kNeedRA;
                 break;
             }

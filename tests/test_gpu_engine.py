@@ -639,3 +639,40 @@ def test_histogram_growth_keeps_the_sweeps(knobs):
         assert res.stats["launches"] >= 3
     finally:
         eng.close()
+
+
+@pytest.mark.parametrize("define", ["-DTRS_B200_LONE=0", "-DTRS_B200_NF_CARRY=0", "-DTRS_B200_PUB_FAST=0"])
+@pytest.mark.parametrize("case", ["reverse64", "fib12", "fibbatch16_s1", "random:3", "random:11"])
+def test_chain_step_switches_are_invisible(engine, case, define, monkeypatch):
+    """The chain-step shortcuts (lone steps, carried nf arguments, unanswered
+    publications) change path length only: with each one
+    compiled out, the reference's rewrites, widths and normal form stay."""
+    monkeypatch.setenv("TRS_B200_JIT_DEFINES", define)
+    if case.startswith("random:"):
+        from oracle import oracle as port
+
+        text = W.random_program(int(case[7:]))
+        o = port.run_text(text)
+        want = (o.rewrites, list(o.widths), list(o.words[0]))
+    else:
+        g = CASES[case]
+        text = g["text"]
+        want = (g["rewrites"], g["widths"], g["words"])
+    res = api.normalize_texts(text, engine=engine)
+    assert res.total_rewrites == want[0]
+    np.testing.assert_array_equal(res.widths, np.asarray(want[1], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(want[2], np.uint32))
+
+
+@pytest.mark.parametrize("past", ["1", "8"])
+@pytest.mark.parametrize("name", ["fibbatch16_s1", "fib12", "treemergesort_2_3_s5"])
+def test_shrinking_phase_handover_is_invisible(engine, name, past, monkeypatch):
+    """An early hand-over to the run-ahead build on a steady frontier past
+    the run's widest sweep (TRS_B200_RA_WARM_PAST) keeps the reference's
+    rewrites, sweeps, widths and normal form."""
+    monkeypatch.setenv("TRS_B200_RA_WARM_PAST", past)
+    g = CASES[name]
+    res = api.normalize_texts(g["text"], engine=engine)
+    assert res.total_rewrites == g["rewrites"] and res.sweeps == g["sweeps"]
+    np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
