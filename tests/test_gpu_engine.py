@@ -676,3 +676,51 @@ def test_shrinking_phase_handover_is_invisible(engine, name, past, monkeypatch):
     assert res.total_rewrites == g["rewrites"] and res.sweeps == g["sweeps"]
     np.testing.assert_array_equal(res.widths, np.asarray(g["widths"], np.uint64))
     np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+
+
+def test_fetch_store_after_capacity_error(engine):
+    """After a Capacity fault the folded bump is clamped to the capacity, so
+    the write-back reads only allocated slots: fetch_store either exports a
+    store within the capacity or reports an error, and the engine stays
+    usable (slab fallback and export after an abort)."""
+    s = api.System(W.mergesort(20, 4))
+    st = api.Store.load(s)
+    v = st.view()
+    engine.set_program(s)
+    cap = v["n"] + 8
+    engine.load(st, capacity=cap)
+    with pytest.raises(api.EngineError) as ei:
+        engine.run(api.make_options(fixed_capacity=1, disable_gc=1, disable_small=1))
+    assert ei.value.fault == api.EngineFault.Capacity
+    try:
+        out = engine.fetch_store(v["maxarity"], v["num_roots"])
+        assert 0 < out["n"] <= cap
+    except api.EngineError:
+        pass
+    g = CASES["fib10"]
+    res = api.normalize_texts(g["text"], engine=engine)
+    assert res.total_rewrites == g["rewrites"]
+    np.testing.assert_array_equal(res.words[0], np.asarray(g["words"], np.uint32))
+
+
+@pytest.mark.parametrize("frac", [0.9, 0.7])
+def test_grid_fixed_capacity_below_slab_room(engine, frac):
+    """Grid sweeps under a fixed capacity that leaves less free room than a
+    slab per active warp: claims are cut at the capacity instead of failing,
+    collections reclaim garbage, and the result is the reference's (or the
+    run stops with Capacity, never with a wrong store)."""
+    g = CASES["fibbatch16_s1"]
+    s = api.System(g["text"])
+    st = api.Store.load(s)
+    engine.set_program(s)
+    engine.load(st)
+    peak = engine.run(api.make_options(disable_gc=1, disable_small=1))["peak_slots"]
+    engine.load(st, capacity=int(peak * frac))
+    try:
+        stats = engine.run(api.make_options(fixed_capacity=1, disable_small=1, validate=1))
+    except api.EngineError as e:
+        assert e.fault == api.EngineFault.Capacity
+        return
+    assert stats["total_rewrites"] == g["rewrites"]
+    np.testing.assert_array_equal(engine.trace()["rewrites"], np.asarray(g["widths"], np.uint64))
+    np.testing.assert_array_equal(engine.canonical(0), np.asarray(g["words"], np.uint32))
