@@ -137,6 +137,8 @@ struct Params {
     uint32_t* val;          // their scratch, 3 words per slot
     uint32_t track_rc;      // steps keep refcounts (validate modes); otherwise collectors recount (gc.cuh)
     uint32_t ra_warm_past;  // hand-over after this many sweeps of a steady frontier past the widest sweep
+    uint32_t warp_max;      // frontiers of at most this many entries run on one warp (1..32; warp_mode)
+    uint32_t warp_max_ra;   // ... in the run-ahead build, whose lanes follow diverging chains
 };
 
 __device__ __forceinline__ uint32_t* region_off(const Params& P, uint32_t buf) {

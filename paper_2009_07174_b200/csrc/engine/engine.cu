@@ -1469,6 +1469,20 @@ int enqueue_launch(trs_gpu_engine* e) {
     P.small_exit = opt.disable_small ? 0 : (opt.small_exit ? opt.small_exit : 2 * kBlock);
     if (P.small_exit < P.small_enter) P.small_exit = P.small_enter;
     P.warp_mode = opt.disable_warp_mode ? 0 : 1;
+    {
+        // Warp mode takes frontiers of up to 32 entries in the lean build
+        // (lanes in step: mergesort 2^14 10 % faster than spreading them over
+        // the CTA's warps), but only single entries in the run-ahead build,
+        // where each lane follows its own chain and a warp of diverging
+        // chains pays for every path (fib(18) 7.9 -> 6.7 ms;
+        // profiles/r2_ab_warpmax.log)
+        const char* wm = std::getenv("TRS_B200_WARP_MAX");  // tuning hooks
+        const char* wr = std::getenv("TRS_B200_WARP_MAX_RA");
+        const uint32_t v = wm ? (uint32_t)std::strtoul(wm, nullptr, 10) : 32u;
+        const uint32_t vr = wr ? (uint32_t)std::strtoul(wr, nullptr, 10) : 1u;
+        P.warp_max = std::min<uint32_t>(std::max<uint32_t>(v, 1u), 32u);
+        P.warp_max_ra = std::min<uint32_t>(std::max<uint32_t>(vr, 1u), 32u);
+    }
     P.gc_interval = opt.gc_interval;
     P.allow_gc = opt.disable_gc ? 0 : 1;
     P.fixed_capacity = opt.fixed_capacity;

@@ -1470,7 +1470,7 @@ __device__ void warp_sweeps(const Params& P, const Prog& G, uint32_t* slist, Sma
     for (;;) {
         const uint32_t sc = ss.sc;
         const uint32_t m = ss.count[sc];
-        if (m == 0 || m > 32) break;
+        if (m == 0 || m > (kRA ? P.warp_max_ra : P.warp_max)) break;
         if (W == 8 && m == 1) {
             // Solo sweeps: while the frontier is a single slot, lane 0 runs
             // sweep after sweep alone -- the warp step without collectives and
@@ -1711,7 +1711,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
             if ((uint64_t)L.bump + (uint64_t)m * P.max_new + 1 > cap / 2) leave_resident();
         }
         if (plan(P, L, m, just_collected, kWarps) != kPlanSweep) break;
-        if (P.warp_mode && m <= 32) {
+        if (P.warp_mode && m <= (kRA ? P.warp_max_ra : P.warp_max)) {
             if (warp == 0) {
                 warp_sweeps<W, kRA>(P, G, slist, ss, L, just_collected, slab, arena, cap, slab_size, tmax);
                 if ((threadIdx.x & 31) == 0) ss.L = L;
@@ -1721,7 +1721,7 @@ __device__ void run_small(const Params& P, const Prog& G, Smem& sm, Local& L, bo
             just_collected = false;
             if (L.total > P.step_budget || ss.flags) break;
             const uint32_t m2 = ss.count[ss.sc];
-            if (m2 <= 32 && !(resident && m2 && (uint64_t)L.bump + (uint64_t)m2 * P.max_new + 1 > cap))
+            if (m2 <= (kRA ? P.warp_max_ra : P.warp_max) && !(resident && m2 && (uint64_t)L.bump + (uint64_t)m2 * P.max_new + 1 > cap))
                 break;  // warp mode stopped for another reason (plan / empty)
             continue;
         }
