@@ -1465,8 +1465,11 @@ int enqueue_launch(trs_gpu_engine* e) {
     const trs_gpu_options& opt = R.opt;
     Params P = make_params(e, R.blocks);
     P.step_budget = opt.step_budget ? opt.step_budget : 1000000000ull;
-    P.small_enter = opt.disable_small ? 0 : (opt.small_enter ? opt.small_enter : kBlock);
-    P.small_exit = opt.disable_small ? 0 : (opt.small_exit ? opt.small_exit : 2 * kBlock);
+    // single-CTA mode below 128 entries, back to the grid above 256
+    // (profiles/r2_opts_ab2.log: build+sum(22) 5.17 -> 5.00 ms against 512 /
+    // 1024, the other configs within 1 %)
+    P.small_enter = opt.disable_small ? 0 : (opt.small_enter ? opt.small_enter : kBlock / 4);
+    P.small_exit = opt.disable_small ? 0 : (opt.small_exit ? opt.small_exit : kBlock / 2);
     if (P.small_exit < P.small_enter) P.small_exit = P.small_enter;
     P.warp_mode = opt.disable_warp_mode ? 0 : 1;
     {
