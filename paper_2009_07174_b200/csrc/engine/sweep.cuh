@@ -159,6 +159,9 @@ constexpr bool kProfBuild = TRS_B200_PROFILE != 0;
 #ifndef TRS_B200_NF_CARRY
 #define TRS_B200_NF_CARRY 1
 #endif
+#ifndef TRS_B200_RA_PREFETCH_LONE
+#define TRS_B200_RA_PREFETCH_LONE 0
+#endif
 #ifndef TRS_B200_RA_PREFETCH
 #define TRS_B200_RA_PREFETCH 1
 #endif
@@ -336,7 +339,8 @@ __device__ __forceinline__ uint32_t warp_step(const Params& P, const Prog& G, ui
         // misses now (words past an arity are slot 0).  Grid sweeps only: the
         // single-CTA modes' chains run from L1 or the resident arena, where
         // the extra instructions measured slower (tools/knob_ab.py)
-        if (kRA && kSolo != 1 && !C.lone && may_cont && C.cont_room && TRS_B200_RA_PREFETCH) {
+        if (kRA && kSolo != 1 && (!C.lone || TRS_B200_RA_PREFETCH_LONE) && may_cont && C.cont_room &&
+            TRS_B200_RA_PREFETCH) {
 #pragma unroll
             for (int q = 0; q < (int)kPlanChildren * 4; ++q)
                 if (ca[q]) asm volatile("prefetch.L1 [%0];" ::"l"(rec<W>(arena, ca[q])));
